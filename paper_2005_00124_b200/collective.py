@@ -1,0 +1,260 @@
+"""Wait-avoiding group allreduce and blocking global allreduce (drop-in for `wagma.collective`).
+
+Same class and method names, arguments, results and errors as the
+reference (`/root/reference/pkg/src/wagma/collective.py`), with the
+simulator slot taken by a `DeviceContext`:
+
+- ``GroupAllreduce(ctx, rank, P, S, on_complete, initial_model, mask_rule,
+  activation_enabled, staleness_bound, contribution_log)``
+- ``install_fresh(vec, iteration)`` / ``join_or_check(version, fresh)``
+- ``SyncAllreduce(ctx, rank, P, on_complete).join(iteration, vec)``
+
+Each join is one device launch of the fused kernel (job kind GROUP_SUM /
+SYNC_SUM): it installs ``fresh`` in the rank's send ring, takes part in
+(or raises) the version's activation, pulls the group's contributions over
+NVLink and returns the accumulator. Ranks hosted by the same process join
+together inside ``with ctx.batch():`` -- one launch for all of them, the
+device analogue of joins that happen at the same simulated instant.
+
+Semantics kept from the reference: exactly-once contribution per (rank,
+version); a member contributes its send buffer as of the activation, so a
+member that joins after the activation is late (``ALREADY_DONE`` with the
+accumulator that already holds its stale contribution; the caller applies
+the S+1 rule, optim.py:443-444); version regression and staleness-bound
+faults; bit-identical sums on every member (fixed butterfly order).
+Deliberate difference: the device does no work on behalf of a rank that
+has not joined, so passive completions are not reported through
+``on_complete``; the late join returns the finished accumulator instead.
+"""
+
+from __future__ import annotations
+
+from contextlib import contextmanager
+from dataclasses import dataclass
+from enum import Enum
+from typing import Callable, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .context import DeviceContext, DeviceProtocolFault, Job
+from .topology import MASK_RULE_EXAMPLE, InvalidParamsError
+
+__all__ = [
+    "ProtocolFault",
+    "VersionRegressionError",
+    "SendBuffer",
+    "JoinStatus",
+    "JoinResult",
+    "GroupAllreduce",
+    "SyncAllreduce",
+    "batch",
+]
+
+
+class ProtocolFault(RuntimeError):
+    """A message/state inconsistent with the protocol (collective.py:65-66)."""
+
+
+class VersionRegressionError(ProtocolFault):
+    """A process tried to join a version at or below one it already joined (collective.py:69-70)."""
+
+
+class JoinStatus(Enum):
+    ACTIVE = "active"
+    ALREADY_DONE = "already_done"
+
+
+@dataclass
+class JoinResult:
+    status: JoinStatus
+    accumulator: Optional[torch.Tensor] = None
+
+
+class SendBuffer:
+    """View of the model snapshot peers pull (collective.py:84-101).
+
+    ``payload`` is the device send-ring slot of the current stamp;
+    ``stamped_iteration`` never decreases.
+    """
+
+    def __init__(self, ctx: DeviceContext, rank: int):
+        self._ctx = ctx
+        self._rank = rank
+        self.stamped_iteration = -1
+
+    @property
+    def payload(self) -> torch.Tensor:
+        view, _ = self._ctx.slot(self._rank, self.stamped_iteration)
+        return view
+
+    def install(self, vec, iteration: int) -> None:
+        if iteration < self.stamped_iteration:
+            raise ProtocolFault(f"send buffer stamp would regress: {self.stamped_iteration} -> {iteration}")
+        self._ctx.install(self._rank, iteration, _as_device(self._ctx, vec))
+        self.stamped_iteration = iteration
+
+
+def _as_device(ctx: DeviceContext, vec) -> torch.Tensor:
+    t = torch.as_tensor(np.asarray(vec) if not isinstance(vec, torch.Tensor) else vec)
+    return t.to(device=ctx.torch_device, dtype=ctx.dtype).contiguous()
+
+
+def _fault(exc: DeviceProtocolFault) -> ProtocolFault:
+    return ProtocolFault(str(exc))
+
+
+class _Pending:
+    def __init__(self, job: Job, resolve: Callable):
+        self.job = job
+        self.resolve = resolve
+
+
+def _submit(ctx: DeviceContext, job: Job, resolve: Callable) -> None:
+    pend = getattr(ctx, "_wg_batch", None)
+    if pend is not None:
+        pend.append(_Pending(job, resolve))
+        return
+    _run(ctx, [_Pending(job, resolve)])
+
+
+def _run(ctx: DeviceContext, items: list[_Pending]) -> None:
+    if not items:
+        return
+    ctx.launch([it.job for it in items])
+    torch.cuda.current_stream(ctx.torch_device).synchronize()
+    try:
+        ctx.check()
+    except DeviceProtocolFault as exc:
+        ctx.clear_error()
+        raise _fault(exc) from exc
+    for it, st in zip(items, ctx.statuses()):
+        it.resolve(st)
+
+
+@contextmanager
+def batch(ctx: DeviceContext):
+    """Collect the joins of several local ranks into one device launch."""
+    if getattr(ctx, "_wg_batch", None) is not None:
+        yield
+        return
+    ctx._wg_batch = []
+    try:
+        yield
+        items = ctx._wg_batch
+    finally:
+        ctx._wg_batch = None
+    _run(ctx, items)
+
+
+DeviceContext.batch = batch  # type: ignore[attr-defined]
+
+
+class GroupAllreduce:
+    """Per-process endpoint of the wait-avoiding group allreduce (collective.py:135-345).
+
+    ``on_complete(version, accumulator, timely, contrib_stamp)`` fires when
+    a join completes in time (from inside ``join_or_check``, or at the end of
+    the enclosing ``ctx.batch()``); a late join returns ``ALREADY_DONE``.
+    With ``activation_enabled=False`` every member waits for the whole group
+    (blocking group allreduce, collective.py:142-145).
+    """
+
+    def __init__(self, ctx: DeviceContext, rank: int, P: int, S: int,
+                 on_complete: Callable[[int, torch.Tensor, bool, int], None], initial_model,
+                 mask_rule: str = MASK_RULE_EXAMPLE, activation_enabled: bool = True,
+                 staleness_bound: Optional[int] = None, contribution_log: Optional[list] = None):
+        if P != ctx.P or S != ctx.S:
+            raise InvalidParamsError(f"endpoint (P={P}, S={S}) differs from its context (P={ctx.P}, S={ctx.S})")
+        if mask_rule != ctx.mask_rule or bool(activation_enabled) != ctx.activation_enabled:
+            raise InvalidParamsError("mask_rule / activation_enabled must match the device context")
+        if rank not in ctx.local_ranks:
+            raise InvalidParamsError(f"rank {rank} is not hosted by this process")
+        self.ctx = ctx
+        self.rank = rank
+        self.P = P
+        self.S = S
+        self.on_complete = on_complete
+        self.mask_rule = mask_rule
+        self.activation_enabled = activation_enabled
+        self.staleness_bound = staleness_bound
+        self.contribution_log = contribution_log
+        self.send_buffer = SendBuffer(ctx, rank)
+        ctx.set_initial_model(rank, _as_device(ctx, initial_model))
+        self.last_joined = -1
+        self.last_completed = -1
+        self.completion_tag = -1
+        self.execution_count: dict[int, int] = {}
+        self.activations_originated = 0
+
+    def install_fresh(self, vec, iteration: int) -> None:
+        self.send_buffer.install(vec, iteration)
+
+    def join_or_check(self, version: int, fresh) -> JoinResult:
+        """Join version ``version`` with the fresh local model (collective.py:192-222)."""
+        if version <= self.last_joined:
+            raise VersionRegressionError(
+                f"rank {self.rank}: join for version {version} after joining {self.last_joined}")
+        if version < self.send_buffer.stamped_iteration:
+            raise ProtocolFault(f"send buffer stamp would regress: {self.send_buffer.stamped_iteration} -> {version}")
+        self.last_joined = version
+        fresh_t = _as_device(self.ctx, fresh)
+        acc = torch.empty_like(fresh_t)
+        result = JoinResult(JoinStatus.ACTIVE)
+        job = Job(rank=self.rank, kind=_lib.WG_JOB_GROUP_SUM, version=version, fresh=fresh_t, acc_out=acc)
+
+        def resolve(st):
+            self.send_buffer.stamped_iteration = version
+            self.execution_count[version] = self.execution_count.get(version, 0) + 1
+            if st.activator:
+                self.activations_originated += 1
+            if self.contribution_log is not None:
+                self.contribution_log.append((self.rank, version, st.contrib_stamp))
+            self.last_completed = max(self.last_completed, version)
+            self.completion_tag = version
+            if st.timely:
+                self.on_complete(version, acc, True, st.contrib_stamp)
+            else:
+                result.status = JoinStatus.ALREADY_DONE
+                result.accumulator = acc
+
+        _submit(self.ctx, job, resolve)
+        return result
+
+
+class SyncAllreduce:
+    """Blocking full-butterfly allreduce over all P processes (collective.py:348-447).
+
+    ``on_complete(iteration, total)`` fires once the bit-identical sum of
+    all P contributions is available.
+    """
+
+    def __init__(self, ctx: DeviceContext, rank: int, P: int, on_complete: Callable[[int, torch.Tensor], None]):
+        if P != ctx.P:
+            raise InvalidParamsError(f"endpoint P={P} differs from its context P={ctx.P}")
+        if rank not in ctx.local_ranks:
+            raise InvalidParamsError(f"rank {rank} is not hosted by this process")
+        self.ctx = ctx
+        self.rank = rank
+        self.P = P
+        self.on_complete = on_complete
+        self.masks = tuple(1 << j for j in range(P.bit_length() - 1))
+        self.last_completed = -1
+        self._joined = -1
+
+    def join(self, iteration: int, vec) -> None:
+        if self._joined > self.last_completed:
+            raise ProtocolFault(f"rank {self.rank}: overlapping sync joins")
+        if iteration <= self.last_completed:
+            raise ProtocolFault(f"rank {self.rank}: sync for iteration {iteration} after {self.last_completed}")
+        self._joined = iteration
+        v = _as_device(self.ctx, vec)
+        total = torch.empty_like(v)
+        job = Job(rank=self.rank, kind=_lib.WG_JOB_SYNC_SUM, version=iteration, fresh=v, acc_out=total)
+
+        def resolve(st):
+            self.last_completed = iteration
+            self.on_complete(iteration, total)
+
+        _submit(self.ctx, job, resolve)

@@ -1,0 +1,1206 @@
+// B200-native WAGMA group-model-averaging hot path (sm_100a).
+//
+// One persistent kernel per launch fuses, tile by tile:
+//   produce  local SGD / momentum step of every job in the launch
+//            (optim.py:176-183), written once into the rank's send-ring slot
+//            (SendBuffer.install, collective.py:95-101) and into shared memory;
+//   publish  per-tile readiness flags (system-scope release) so peers on other
+//            GPUs can pull the tile over NVLink as soon as it exists;
+//   consume  the group sum: S leaves pulled with 128-bit loads from peer
+//            send-ring slots (NVLink / NVSwitch) or from shared memory, summed
+//            in the butterfly tree order of the reference's recursive doubling
+//            (collective.py:310-329), then divided by S (timely), S+1 (late,
+//            optim.py:439-447) or P (global sync, optim.py:449-452).
+//
+// The wait-avoiding activation (collective.py:192-308) is one activation
+// descriptor per version on GPU 0: the first rank to arrive CASes it
+// (system scope), waits at most a grace window for the other ranks to
+// announce, locks every rank's contribution stamp (its latest announced
+// version: fresh W' if it joined, its last-published stale W' otherwise) and
+// releases it. No host round trip, no global barrier; only the periodic
+// global sync (S = P, blocking) waits for everyone.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/wagma_b200.h"
+#include "wagma_internal.h"
+
+namespace wg {
+
+// ---------------------------------------------------------------------------
+// error reporting
+// ---------------------------------------------------------------------------
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+static int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define WG_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(WG_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_));           \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// device-memory arena (one per GPU, exported to peers with CUDA IPC)
+// ---------------------------------------------------------------------------
+
+struct Desc {                 // activation descriptor of one group version
+    int64_t state;            // 0 free; (v+1)*4+1 locking; (v+1)*4+2 locked
+    int64_t pad[15];
+    int64_t stamps[kMaxP];    // contribution stamp of every rank
+};
+
+struct Layout {
+    int64_t hdr;       // int64 error code, int64 error info
+    int64_t announce;  // int64 [R] (128-byte stride): latest announced version
+    int64_t complete;  // int64 [R][D]: stamp whose tiles are all published
+    int64_t counter;   // uint32 [R][D]: tiles published for the current stamp
+    int64_t desc;      // Desc [Dv]  (used on GPU 0 only)
+    int64_t flags;     // int64 [R][D][n_tiles]: stamp held by each slot tile
+    int64_t ring;      // T [R][D][npad]: send ring
+    int64_t total;
+};
+
+constexpr int kAnnounceStride = 16;  // int64 words (128 B)
+constexpr int64_t kNever = INT64_MIN / 2;
+
+enum VersionMode : int32_t { kLive = 0, kForced = 1, kBlocking = 2, kSync = 3 };
+
+struct DevJob {
+    int32_t rank, local, kind, update_rule;
+    int64_t version;
+    int32_t vidx, plan, produces, pad;
+    double eta, beta;
+    void* W;
+    void* m;
+    const void* g;
+    const void* fresh;
+    void* acc_out;
+};
+
+struct DevVersion {
+    int64_t version;
+    int32_t mode, forced_idx;
+};
+
+struct DevPlan {
+    int32_t vidx, n_leaves, log_leaves, divisor, n_members, pad;
+    int16_t leaves[kMaxLeaves];
+    int8_t members[kMaxJobs];
+};
+
+struct LaunchParams {
+    char* base[kMaxGpus];
+    Layout L;
+    int32_t P, S, R, G, gpu_index, D, Dv, n_jobs, n_versions, n_plans, need_fence, pad;
+    int64_t n, npad, n_tiles, tile_elems;
+    int64_t grace_ns, timeout_ns, staleness_bound;
+    int32_t job_of_rank[kMaxP];
+    DevJob jobs[kMaxJobs];
+    DevVersion versions[kMaxVersions];
+    DevPlan plans[kMaxPlans];
+    int64_t forced[kMaxVersions][kMaxP];
+    wg_job_status* status;
+};
+
+// ---------------------------------------------------------------------------
+// device helpers: scoped memory operations (PTX memory model)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t* p) {
+    int64_t v;
+    asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int64_t ld_relaxed_sys(const int64_t* p) {
+    int64_t v;
+    asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(int64_t* p, int64_t v) {
+    asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(int64_t* p, int64_t v) {
+    asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int64_t atom_cas_sys(int64_t* p, int64_t cmp, int64_t val) {
+    int64_t old;
+    asm volatile("atom.acq_rel.sys.global.cas.b64 %0, [%1], %2, %3;"
+                 : "=l"(old)
+                 : "l"(p), "l"(cmp), "l"(val)
+                 : "memory");
+    return old;
+}
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// element traits: 16-byte vectors, IEEE round-to-nearest ops (no contraction)
+// ---------------------------------------------------------------------------
+
+template <typename T>
+struct Tr;
+template <>
+struct Tr<float> {
+    using V = float4;
+    static constexpr int EPV = 4;
+};
+template <>
+struct Tr<double> {
+    using V = double2;
+    static constexpr int EPV = 2;
+};
+
+__device__ __forceinline__ float4 vadd(float4 a, float4 b) {
+    return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 vsub(float4 a, float4 b) {
+    return make_float4(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y), __fsub_rn(a.z, b.z), __fsub_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 vscale(float s, float4 a) {
+    return make_float4(__fmul_rn(s, a.x), __fmul_rn(s, a.y), __fmul_rn(s, a.z), __fmul_rn(s, a.w));
+}
+__device__ __forceinline__ float4 vdiv(float4 a, float d) {
+    return make_float4(__fdiv_rn(a.x, d), __fdiv_rn(a.y, d), __fdiv_rn(a.z, d), __fdiv_rn(a.w, d));
+}
+__device__ __forceinline__ double2 vadd(double2 a, double2 b) {
+    return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ double2 vsub(double2 a, double2 b) {
+    return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
+}
+__device__ __forceinline__ double2 vscale(double s, double2 a) {
+    return make_double2(__dmul_rn(s, a.x), __dmul_rn(s, a.y));
+}
+__device__ __forceinline__ double2 vdiv(double2 a, double d) {
+    return make_double2(__ddiv_rn(a.x, d), __ddiv_rn(a.y, d));
+}
+
+// Caller-owned vectors (W, m, g, fresh, acc_out) have exactly n elements:
+// full 16-byte vectors inside, element-wise handling of the ragged end.
+template <typename T>
+__device__ __forceinline__ typename Tr<T>::V ld_stream(const T* base, int64_t idx, int64_t n) {
+    using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
+    if (idx + E <= n) return __ldcs(reinterpret_cast<const V*>(base + idx));
+    V v;
+    T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+    for (int i = 0; i < E; ++i) e[i] = (idx + i < n) ? base[idx + i] : T(0);
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ void st_stream(T* base, int64_t idx, int64_t n, typename Tr<T>::V v) {
+    using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
+    if (idx + E <= n) {
+        __stcs(reinterpret_cast<V*>(base + idx), v);
+        return;
+    }
+    const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+        if (idx + i < n) base[idx + i] = e[i];
+}
+
+// ---------------------------------------------------------------------------
+// arena addressing (rank r lives on GPU r / R at local index r % R)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ char* rank_base(const LaunchParams& p, int rank) { return p.base[rank / p.R]; }
+__device__ __forceinline__ int64_t* announce_ptr(const LaunchParams& p, int rank) {
+    return reinterpret_cast<int64_t*>(rank_base(p, rank) + p.L.announce) + (rank % p.R) * kAnnounceStride;
+}
+__device__ __forceinline__ int slot_of(const LaunchParams& p, int64_t stamp) {
+    return int((stamp + 1) % p.D);
+}
+__device__ __forceinline__ int64_t* complete_ptr(const LaunchParams& p, int rank, int slot) {
+    return reinterpret_cast<int64_t*>(rank_base(p, rank) + p.L.complete) + (rank % p.R) * p.D + slot;
+}
+__device__ __forceinline__ unsigned* counter_ptr(const LaunchParams& p, int rank, int slot) {
+    return reinterpret_cast<unsigned*>(rank_base(p, rank) + p.L.counter) + (rank % p.R) * p.D + slot;
+}
+__device__ __forceinline__ int64_t* flag_ptr(const LaunchParams& p, int rank, int slot, int64_t tile) {
+    return reinterpret_cast<int64_t*>(rank_base(p, rank) + p.L.flags) +
+           ((int64_t(rank % p.R) * p.D + slot) * p.n_tiles + tile);
+}
+template <typename T>
+__device__ __forceinline__ T* ring_ptr(const LaunchParams& p, int rank, int slot) {
+    return reinterpret_cast<T*>(rank_base(p, rank) + p.L.ring) + (int64_t(rank % p.R) * p.D + slot) * p.npad;
+}
+__device__ __forceinline__ Desc* desc_ptr(const LaunchParams& p, int64_t version) {
+    return reinterpret_cast<Desc*>(p.base[0] + p.L.desc) + (version % p.Dv);
+}
+__device__ __forceinline__ int64_t* err_ptr(const LaunchParams& p) {
+    return reinterpret_cast<int64_t*>(p.base[p.gpu_index] + p.L.hdr);
+}
+
+__device__ __noinline__ void raise_error(const LaunchParams& p, int code, int64_t info) {
+    int64_t* e = err_ptr(p);
+    if (atomicCAS(reinterpret_cast<unsigned long long*>(e), 0ull, (unsigned long long)code) == 0ull)
+        e[1] = info;
+    __threadfence_system();
+}
+__device__ __forceinline__ bool aborted(const LaunchParams& p) {
+    return ld_relaxed_sys(err_ptr(p)) != 0;
+}
+
+// Spin until *addr == want. Returns 0 ok, WG_EPROTO if the word moved past
+// `want` (slot reused / descriptor recycled), WG_ETIMEOUT on the watchdog.
+__device__ int spin_eq(const LaunchParams& p, const int64_t* addr, int64_t want, uint64_t t0) {
+    int64_t v = ld_acquire_sys(addr);
+    int it = 0;
+    while (v != want) {
+        if (v > want) return WG_EPROTO;
+        if ((++it & 63) == 0) {
+            if (globaltimer() - t0 > uint64_t(p.timeout_ns)) return WG_ETIMEOUT;
+            if (aborted(p)) return WG_ETIMEOUT;
+        }
+        __nanosleep(64);
+        v = ld_acquire_sys(addr);
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// control phase (CTA 0, warp 0): announce, activation, lock-in
+// ---------------------------------------------------------------------------
+
+__device__ void control_phase(const LaunchParams& p, int* s_activator) {
+    const int lane = threadIdx.x & 31;
+    // Announce "rank r is producing W'_v in a running kernel" (the join,
+    // collective.py:192-205). Activators lock contribution stamps from it.
+    if (lane == 0) {
+        for (int j = 0; j < p.n_jobs; ++j)
+            if (p.jobs[j].produces) st_release_sys(announce_ptr(p, p.jobs[j].rank), p.jobs[j].version);
+        fence_sys();
+    }
+    __syncwarp();
+    for (int vi = 0; vi < p.n_versions; ++vi) {
+        if (lane == 0) s_activator[vi] = 0;
+        if (p.versions[vi].mode != kLive) continue;
+        const int64_t v = p.versions[vi].version;
+        Desc* d = desc_ptr(p, v);
+        int act = 0;
+        if (lane == 0) {
+            // First arrival raises the activation flag (collective.py:214-218);
+            // later arrivals find it raised (exactly-once, collective.py:236).
+            int64_t st = ld_acquire_sys(&d->state);
+            for (;;) {
+                const int64_t sv = st / 4 - 1;
+                if (sv == v) break;
+                if (sv > v) {  // descriptor recycled before this join
+                    raise_error(p, WG_EPROTO, v);
+                    break;
+                }
+                const int64_t old = atom_cas_sys(&d->state, st, (v + 1) * 4 + 1);
+                if (old == st) {
+                    act = 1;
+                    break;
+                }
+                st = old;
+            }
+        }
+        act = __shfl_sync(0xffffffffu, act, 0);
+        if (!act) continue;
+        if (lane == 0) s_activator[vi] = 1;
+        // Bounded grace window: ranks on other GPUs that join within it are
+        // timely. Ranks on this GPU announced at launch start (final).
+        const uint64_t t0 = globaltimer();
+        const int q0 = lane, q1 = lane + 32;
+        int64_t a0 = kNever, a1 = kNever;
+        for (;;) {
+            bool in = true;
+            if (q0 < p.P) {
+                a0 = ld_acquire_sys(announce_ptr(p, q0));
+                if (a0 < v && q0 / p.R != p.gpu_index) in = false;
+            }
+            if (q1 < p.P) {
+                a1 = ld_acquire_sys(announce_ptr(p, q1));
+                if (a1 < v && q1 / p.R != p.gpu_index) in = false;
+            }
+            if (__all_sync(0xffffffffu, in)) break;
+            if (globaltimer() - t0 > uint64_t(p.grace_ns)) break;
+            __nanosleep(200);
+        }
+        // Lock-in (collective.py:289-301): each rank contributes its latest
+        // announced W' -- fresh if it joined v, its stale send buffer if not.
+        if (q0 < p.P) {
+            const int64_t s = a0 < v ? a0 : v;
+            d->stamps[q0] = s;
+            if (p.staleness_bound > 0 && s <= v - p.staleness_bound)
+                raise_error(p, WG_ESTALE, v * 1024 + q0);  // collective.py:290-294
+        }
+        if (q1 < p.P) {
+            const int64_t s = a1 < v ? a1 : v;
+            d->stamps[q1] = s;
+            if (p.staleness_bound > 0 && s <= v - p.staleness_bound) raise_error(p, WG_ESTALE, v * 1024 + q1);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            fence_sys();
+            st_release_sys(&d->state, (v + 1) * 4 + 2);
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// per-CTA shared state
+// ---------------------------------------------------------------------------
+
+enum LeafSrc : int8_t { kSrcPoll = -1, kSrcReady = -2 };
+
+struct SmemCtl {
+    int64_t stamps[kMaxVersions][kMaxP];     // contribution stamps per version
+    const void* leaf_ptr[kMaxPlans][kMaxLeaves];
+    int8_t leaf_src[kMaxPlans][kMaxLeaves];  // >=0: stage of job; -1 poll; -2 ready
+    int16_t leaf_slot[kMaxPlans][kMaxLeaves];
+    int32_t plan_polls[kMaxPlans];
+    int32_t activator[kMaxVersions];
+    int32_t abort;
+};
+
+// Resolve every plan's leaves to a source once per CTA (after lock-in).
+template <typename T>
+__device__ bool resolve_sources(const LaunchParams& p, SmemCtl& sm) {
+    const int tid = threadIdx.x;
+    const uint64_t t0 = globaltimer();
+    if (tid == 0) {
+        for (int vi = 0; vi < p.n_versions && !sm.abort; ++vi) {
+            if (p.versions[vi].mode != kLive) continue;
+            const int64_t v = p.versions[vi].version;
+            const int rc = spin_eq(p, &desc_ptr(p, v)->state, (v + 1) * 4 + 2, t0);
+            if (rc) {
+                raise_error(p, rc, v);
+                sm.abort = 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (sm.abort) return false;
+    for (int i = tid; i < p.n_versions * p.P; i += blockDim.x) {
+        const int vi = i / p.P, q = i % p.P;
+        const DevVersion& dv = p.versions[vi];
+        int64_t s;
+        if (dv.mode == kLive)
+            s = ld_relaxed_sys(&desc_ptr(p, dv.version)->stamps[q]);
+        else if (dv.mode == kForced)
+            s = p.forced[dv.forced_idx][q];
+        else
+            s = dv.version;
+        sm.stamps[vi][q] = s;
+    }
+    __syncthreads();
+    for (int i = tid; i < p.n_plans * kMaxLeaves; i += blockDim.x) {
+        const int pl = i / kMaxLeaves, li = i % kMaxLeaves;
+        const DevPlan& P_ = p.plans[pl];
+        if (li >= P_.n_leaves) continue;
+        const int q = P_.leaves[li];
+        const int64_t s = sm.stamps[P_.vidx][q];
+        const int j = p.job_of_rank[q];
+        int8_t src;
+        if (s < -1) {
+            raise_error(p, WG_EPROTO, q);
+            sm.abort = 1;
+            src = kSrcReady;
+        } else if (j >= 0 && p.jobs[j].produces && p.jobs[j].version == s) {
+            src = int8_t(j);  // produced by this launch: shared-memory stage
+        } else {
+            const int slot = slot_of(p, s);
+            if (j >= 0 && p.jobs[j].produces && slot_of(p, p.jobs[j].version) == slot) {
+                raise_error(p, WG_EPROTO, s);  // slot overwritten in this launch
+                sm.abort = 1;
+            }
+            const int64_t c = ld_acquire_sys(complete_ptr(p, q, slot));
+            if (c > s) {
+                raise_error(p, WG_EPROTO, s);  // send ring wrapped past the stamp
+                sm.abort = 1;
+            }
+            src = (c == s) ? int8_t(kSrcReady) : int8_t(kSrcPoll);
+            sm.leaf_ptr[pl][li] = ring_ptr<T>(p, q, slot);
+            sm.leaf_slot[pl][li] = int16_t(slot);
+        }
+        sm.leaf_src[pl][li] = src;
+    }
+    __syncthreads();
+    if (tid < p.n_plans) {
+        int polls = 0;
+        for (int li = 0; li < p.plans[tid].n_leaves; ++li) polls |= (sm.leaf_src[tid][li] == kSrcPoll);
+        sm.plan_polls[tid] = polls;
+    }
+    __syncthreads();
+    return !sm.abort;
+}
+
+// ---------------------------------------------------------------------------
+// produce: local step, send-ring install, shared-memory stage
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__device__ __forceinline__ void produce_tile(const LaunchParams& p, int64_t tile, typename Tr<T>::V* stage) {
+    using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
+    constexpr int U = kVecPerThread;
+    const int tid = threadIdx.x;
+    const int64_t tbase = tile * p.tile_elems;
+    for (int j = 0; j < p.n_jobs; ++j) {
+        const DevJob& jb = p.jobs[j];
+        V wp[U];
+        if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
+            const T* fr = static_cast<const T*>(jb.fresh);
+#pragma unroll
+            for (int k = 0; k < U; ++k) wp[k] = ld_stream<T>(fr, tbase + int64_t(k * kThreads + tid) * E, p.n);
+        } else {
+            T* W = static_cast<T*>(jb.W);
+            const T* g = static_cast<const T*>(jb.g);
+            const T eta = T(jb.eta);
+            V w[U], gv[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int64_t idx = tbase + int64_t(k * kThreads + tid) * E;
+                w[k] = ld_stream<T>(W, idx, p.n);
+                gv[k] = ld_stream<T>(g, idx, p.n);
+            }
+            if (jb.update_rule == WG_UPDATE_MOMENTUM) {
+                // m = beta*m + g ; W' = W - eta*m  (optim.py:179,183)
+                T* m = static_cast<T*>(jb.m);
+                const T beta = T(jb.beta);
+                V mv[U];
+#pragma unroll
+                for (int k = 0; k < U; ++k) mv[k] = ld_stream<T>(m, tbase + int64_t(k * kThreads + tid) * E, p.n);
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    const V mn = vadd(vscale(beta, mv[k]), gv[k]);
+                    st_stream<T>(m, tbase + int64_t(k * kThreads + tid) * E, p.n, mn);
+                    wp[k] = vsub(w[k], vscale(eta, mn));
+                }
+            } else {
+                // W' = W - eta*g  (optim.py:181-183)
+#pragma unroll
+                for (int k = 0; k < U; ++k) wp[k] = vsub(w[k], vscale(eta, gv[k]));
+            }
+            if (jb.kind == WG_JOB_LOCAL_STEP) {
+#pragma unroll
+                for (int k = 0; k < U; ++k) st_stream<T>(W, tbase + int64_t(k * kThreads + tid) * E, p.n, wp[k]);
+                continue;
+            }
+        }
+        // SendBuffer.install (collective.py:95-101): one write into the ring
+        T* slot = ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + tbase;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            __stcg(reinterpret_cast<V*>(slot + int64_t(k * kThreads + tid) * E), wp[k]);
+            stage[(j * U + k) * kThreads + tid] = wp[k];
+        }
+    }
+}
+
+__device__ __forceinline__ void publish_tile(const LaunchParams& p, int64_t tile) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (p.need_fence) fence_sys();  // CTA's tile stores visible to peers first
+        for (int j = 0; j < p.n_jobs; ++j) {
+            const DevJob& jb = p.jobs[j];
+            if (!jb.produces) continue;
+            const int slot = slot_of(p, jb.version);
+            st_relaxed_sys(flag_ptr(p, jb.rank, slot, tile), jb.version);
+        }
+        for (int j = 0; j < p.n_jobs; ++j) {
+            const DevJob& jb = p.jobs[j];
+            if (!jb.produces) continue;
+            const int slot = slot_of(p, jb.version);
+            unsigned* c = counter_ptr(p, jb.rank, slot);
+            if (atomicAdd(c, 1u) == unsigned(p.n_tiles - 1)) {
+                *c = 0u;  // last tile of this stamp: whole slot published
+                fence_sys();
+                st_release_sys(complete_ptr(p, jb.rank, slot), jb.version);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// consume: butterfly-tree sum of the group's leaves, averaging rule
+// ---------------------------------------------------------------------------
+
+template <typename T, int LOG>
+struct TreeSum {
+    using V = typename Tr<T>::V;
+    static __device__ __forceinline__ void run(const SmemCtl& sm, int pl, int leaf0, int64_t toff,
+                                               const V* stage, V* out) {
+        V a[kVecPerThread], b[kVecPerThread];
+        TreeSum<T, LOG - 1>::run(sm, pl, leaf0, toff, stage, a);
+        TreeSum<T, LOG - 1>::run(sm, pl, leaf0 + (1 << (LOG - 1)), toff, stage, b);
+#pragma unroll
+        for (int k = 0; k < kVecPerThread; ++k) out[k] = vadd(a[k], b[k]);
+    }
+};
+template <typename T>
+struct TreeSum<T, 0> {
+    using V = typename Tr<T>::V;
+    static __device__ __forceinline__ void run(const SmemCtl& sm, int pl, int leaf, int64_t toff,
+                                               const V* stage, V* out) {
+        constexpr int E = Tr<T>::EPV;
+        const int src = sm.leaf_src[pl][leaf];
+        const int tid = threadIdx.x;
+        if (src >= 0) {
+#pragma unroll
+            for (int k = 0; k < kVecPerThread; ++k) out[k] = stage[(src * kVecPerThread + k) * kThreads + tid];
+        } else {
+            // 128-bit loads of a peer's (NVLink) or an older local send slot;
+            // .cg: L2 only, never a stale L1 line of a re-published slot.
+            const T* base = static_cast<const T*>(sm.leaf_ptr[pl][leaf]) + toff;
+#pragma unroll
+            for (int k = 0; k < kVecPerThread; ++k)
+                out[k] = __ldcg(reinterpret_cast<const V*>(base + int64_t(k * kThreads + tid) * E));
+        }
+    }
+};
+
+template <typename T>
+__device__ __forceinline__ void tree_sum(const SmemCtl& sm, int pl, int log_leaves, int64_t toff,
+                                         const typename Tr<T>::V* stage, typename Tr<T>::V* out) {
+    switch (log_leaves) {
+        case 0: TreeSum<T, 0>::run(sm, pl, 0, toff, stage, out); break;
+        case 1: TreeSum<T, 1>::run(sm, pl, 0, toff, stage, out); break;
+        case 2: TreeSum<T, 2>::run(sm, pl, 0, toff, stage, out); break;
+        case 3: TreeSum<T, 3>::run(sm, pl, 0, toff, stage, out); break;
+        case 4: TreeSum<T, 4>::run(sm, pl, 0, toff, stage, out); break;
+        case 5: TreeSum<T, 5>::run(sm, pl, 0, toff, stage, out); break;
+        default: TreeSum<T, 6>::run(sm, pl, 0, toff, stage, out); break;
+    }
+}
+
+template <typename T>
+__device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, const typename Tr<T>::V* stage) {
+    using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
+    constexpr int U = kVecPerThread;
+    const int tid = threadIdx.x;
+    const int64_t tbase = tile * p.tile_elems;
+    for (int pl = 0; pl < p.n_plans; ++pl) {
+        const DevPlan& P_ = p.plans[pl];
+        if (sm.plan_polls[pl]) {
+            // wait for the tiles peers are still producing (per-tile flags)
+            if (tid < P_.n_leaves && sm.leaf_src[pl][tid] == kSrcPoll) {
+                const int q = P_.leaves[tid];
+                const int64_t s = sm.stamps[P_.vidx][q];
+                const int rc = spin_eq(p, flag_ptr(p, q, sm.leaf_slot[pl][tid], tile), s, globaltimer());
+                if (rc) {
+                    raise_error(p, rc, int64_t(q) << 32 | (tile & 0xffffffff));
+                    sm.abort = 1;
+                }
+            }
+            __syncthreads();
+            if (sm.abort) return false;
+        }
+        V acc[U];
+        tree_sum<T>(sm, pl, P_.log_leaves, tbase, stage, acc);
+        for (int mi = 0; mi < P_.n_members; ++mi) {
+            const int j = P_.members[mi];
+            const DevJob& jb = p.jobs[j];
+            if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
+                T* out = static_cast<T*>(jb.acc_out);
+#pragma unroll
+                for (int k = 0; k < U; ++k) st_stream<T>(out, tbase + int64_t(k * kThreads + tid) * E, p.n, acc[k]);
+                continue;
+            }
+            T* W = static_cast<T*>(jb.W);
+            const bool timely = jb.kind == WG_JOB_SYNC_STEP || sm.stamps[jb.vidx][jb.rank] == jb.version;
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                V out;
+                if (timely) {
+                    out = vdiv(acc[k], T(P_.divisor));  // acc/S, total/P (optim.py:442,452)
+                } else {
+                    // late member: (acc + W')/(S+1)  (optim.py:443-444)
+                    out = vdiv(vadd(acc[k], stage[(j * U + k) * kThreads + tid]), T(P_.divisor + 1));
+                }
+                st_stream<T>(W, tbase + int64_t(k * kThreads + tid) * E, p.n, out);
+            }
+        }
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// the fused step kernel (persistent: grid <= co-resident CTAs)
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 2) wagma_step_kernel(const __grid_constant__ LaunchParams p) {
+    using V = typename Tr<T>::V;
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
+    V* stage = reinterpret_cast<V*>(dyn_smem);
+    __shared__ SmemCtl sm;
+    if (threadIdx.x == 0) sm.abort = 0;
+    if (threadIdx.x < kMaxVersions) sm.activator[threadIdx.x] = 0;
+    __syncthreads();
+    if (blockIdx.x == 0) {
+        if (threadIdx.x < 32) control_phase(p, sm.activator);
+        __syncthreads();
+    }
+    bool resolved = false;
+    for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        produce_tile<T>(p, tile, stage);
+        publish_tile(p, tile);
+        if (!resolved) {
+            if (!resolve_sources<T>(p, sm)) break;
+            resolved = true;
+        }
+        if (!consume_tile<T>(p, sm, tile, stage)) break;
+    }
+    if (blockIdx.x == 0) {
+        if (!resolved && !sm.abort) resolved = resolve_sources<T>(p, sm);
+        __syncthreads();
+        if (threadIdx.x < p.n_jobs) {
+            const DevJob& jb = p.jobs[threadIdx.x];
+            wg_job_status st;
+            st.version = jb.version;
+            st.contrib_stamp = (jb.kind == WG_JOB_LOCAL_STEP || !resolved) ? jb.version : sm.stamps[jb.vidx][jb.rank];
+            st.timely = st.contrib_stamp == jb.version;
+            st.activator = jb.vidx >= 0 ? sm.activator[jb.vidx] : 0;
+            st.error = int32_t(ld_relaxed_sys(err_ptr(p)));
+            st.pad = 0;
+            p.status[threadIdx.x] = st;
+        }
+    }
+}
+
+__global__ void fill_i64_kernel(int64_t* p, int64_t n, int64_t v) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) p[i] = v;
+}
+
+__global__ void delay_kernel(int64_t ns) {
+    const uint64_t t0 = globaltimer();
+    while (globaltimer() - t0 < uint64_t(ns)) __nanosleep(1000);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+static bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+static int ilog2(int64_t n) {
+    int r = 0;
+    while ((int64_t(1) << (r + 1)) <= n) ++r;
+    return r;
+}
+
+struct Blob {
+    uint64_t magic;
+    int32_t gpu_index, P, R, D, Dv, dtype;
+    int64_t n, arena_bytes;
+    cudaIpcMemHandle_t handle;
+};
+constexpr uint64_t kBlobMagic = 0x57474d4142323030ull;  // "WGMAB200"
+
+}  // namespace wg
+
+using namespace wg;
+
+struct wg_ctx {
+    wg_config cfg;
+    int R, D, Dv;
+    size_t esize;
+    int64_t tile_elems, n_tiles, npad;
+    Layout L;
+    char* base[kMaxGpus];
+    bool opened[kMaxGpus];
+    char* arena;
+    wg_job_status* status_host;
+    wg_job_status* status_dev;
+    int last_n_jobs;
+    int sms;
+    int occ[kMaxJobs + 1];
+};
+
+extern "C" {
+
+const char* wg_strerror(int code) {
+    switch (code) {
+        case WG_OK: return "ok";
+        case WG_EINVAL: return "invalid parameters";
+        case WG_EVERSION: return "version regression";
+        case WG_ESTALE: return "stale contribution violates staleness bound";
+        case WG_EPROTO: return "protocol fault";
+        case WG_ETIMEOUT: return "device watchdog timeout (peer never published)";
+        case WG_ECUDA: return "CUDA runtime error";
+        case WG_ENOMEM: return "out of memory";
+        default: return "unknown error";
+    }
+}
+
+const char* wg_last_error_message(void) { return g_last_error.c_str(); }
+
+int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
+    if (!cfg || !out) return fail(WG_EINVAL, "null argument");
+    const wg_config& c = *cfg;
+    if (!is_pow2(c.P) || c.P > kMaxP) return fail(WG_EINVAL, "P=%d must be a power of two <= %d", c.P, kMaxP);
+    if (!is_pow2(c.S) || c.S > c.P) return fail(WG_EINVAL, "S=%d must be a power of two <= P", c.S);
+    if (c.n_gpus < 1 || c.n_gpus > kMaxGpus || c.P % c.n_gpus)
+        return fail(WG_EINVAL, "n_gpus=%d must divide P and be <= %d", c.n_gpus, kMaxGpus);
+    if (c.gpu_index < 0 || c.gpu_index >= c.n_gpus) return fail(WG_EINVAL, "gpu_index out of range");
+    if (c.P / c.n_gpus > kMaxJobs) return fail(WG_EINVAL, "at most %d ranks per GPU", kMaxJobs);
+    if (c.dtype != WG_F32 && c.dtype != WG_F64) return fail(WG_EINVAL, "dtype");
+    if (c.mask_rule != WG_RULE_EXAMPLE && c.mask_rule != WG_RULE_LITERAL) return fail(WG_EINVAL, "mask rule");
+    if (c.n < 0 || c.tau < 0) return fail(WG_EINVAL, "n and tau must be >= 0");
+    wg_ctx* ctx = new wg_ctx();
+    std::memset(ctx, 0, sizeof(*ctx));
+    ctx->cfg = c;
+    if (ctx->cfg.grace_ns <= 0) ctx->cfg.grace_ns = 100000;
+    if (ctx->cfg.timeout_ns <= 0) ctx->cfg.timeout_ns = 20000000000ll;
+    ctx->R = c.P / c.n_gpus;
+    ctx->D = c.ring_depth > 0 ? c.ring_depth : (c.tau > 0 ? int(std::max<int64_t>(2 * c.tau, 4)) : 16);
+    ctx->Dv = c.version_ring > 0 ? c.version_ring : (c.tau > 0 ? int(std::max<int64_t>(2 * c.tau, 8)) : 64);
+    if (ctx->D < 2 || ctx->D > 32767) {
+        delete ctx;
+        return fail(WG_EINVAL, "ring depth");
+    }
+    ctx->esize = c.dtype == WG_F32 ? 4 : 8;
+    ctx->tile_elems = int64_t(kThreads) * kVecPerThread * (16 / int64_t(ctx->esize));
+    ctx->n_tiles = std::max<int64_t>(1, (c.n + ctx->tile_elems - 1) / ctx->tile_elems);
+    ctx->npad = ctx->n_tiles * ctx->tile_elems;
+    Layout& L = ctx->L;
+    int64_t off = 0;
+    L.hdr = off;
+    off = align_up(off + 256, 256);
+    L.announce = off;
+    off = align_up(off + int64_t(ctx->R) * kAnnounceStride * 8, 256);
+    L.complete = off;
+    off = align_up(off + int64_t(ctx->R) * ctx->D * 8, 256);
+    L.counter = off;
+    off = align_up(off + int64_t(ctx->R) * ctx->D * 4, 256);
+    L.desc = off;
+    off = align_up(off + int64_t(ctx->Dv) * int64_t(sizeof(Desc)), 256);
+    L.flags = off;
+    off = align_up(off + int64_t(ctx->R) * ctx->D * ctx->n_tiles * 8, 4096);
+    L.ring = off;
+    off = align_up(off + int64_t(ctx->R) * ctx->D * ctx->npad * int64_t(ctx->esize), 4096);
+    L.total = off;
+
+    int rc = WG_OK;
+    do {
+        cudaError_t e = cudaSetDevice(c.device);
+        if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaSetDevice(%d): %s", c.device, cudaGetErrorString(e)); break; }
+        e = cudaMalloc(&ctx->arena, size_t(L.total));
+        if (e != cudaSuccess) { rc = fail(WG_ENOMEM, "cudaMalloc(%lld): %s", (long long)L.total, cudaGetErrorString(e)); break; }
+        e = cudaMemset(ctx->arena, 0, size_t(L.ring));
+        if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaMemset: %s", cudaGetErrorString(e)); break; }
+        auto fill = [&](int64_t byte_off, int64_t count, int64_t v) {
+            if (count <= 0) return;
+            fill_i64_kernel<<<256, 256>>>(reinterpret_cast<int64_t*>(ctx->arena + byte_off), count, v);
+        };
+        fill(L.announce, int64_t(ctx->R) * kAnnounceStride, -1);
+        fill(L.complete, int64_t(ctx->R) * ctx->D, kNever);
+        fill(L.flags, int64_t(ctx->R) * ctx->D * ctx->n_tiles, kNever);
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { rc = fail(WG_ECUDA, "arena init: %s", cudaGetErrorString(e)); break; }
+        e = cudaHostAlloc(&ctx->status_host, sizeof(wg_job_status) * kMaxJobs, cudaHostAllocMapped);
+        if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaHostAlloc: %s", cudaGetErrorString(e)); break; }
+        std::memset(ctx->status_host, 0, sizeof(wg_job_status) * kMaxJobs);
+        e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->status_dev), ctx->status_host, 0);
+        if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e)); break; }
+        const int max_smem = kMaxJobs * kThreads * kVecPerThread * 16;
+        e = cudaFuncSetAttribute(wagma_step_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(wagma_step_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+        if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)); break; }
+        e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, c.device);
+        if (e != cudaSuccess) { rc = fail(WG_ECUDA, "device attribute: %s", cudaGetErrorString(e)); break; }
+    } while (0);
+    if (rc != WG_OK) {
+        if (ctx->arena) cudaFree(ctx->arena);
+        if (ctx->status_host) cudaFreeHost(ctx->status_host);
+        delete ctx;
+        return rc;
+    }
+    ctx->base[c.gpu_index] = ctx->arena;
+    ctx->opened[c.gpu_index] = false;
+    *out = ctx;
+    return WG_OK;
+}
+
+int wg_ctx_destroy(wg_ctx* ctx) {
+    if (!ctx) return WG_OK;
+    cudaSetDevice(ctx->cfg.device);
+    cudaDeviceSynchronize();
+    for (int g = 0; g < kMaxGpus; ++g)
+        if (ctx->opened[g] && ctx->base[g]) cudaIpcCloseMemHandle(ctx->base[g]);
+    if (ctx->arena) cudaFree(ctx->arena);
+    if (ctx->status_host) cudaFreeHost(ctx->status_host);
+    delete ctx;
+    return WG_OK;
+}
+
+int wg_ctx_export(wg_ctx* ctx, void* blob, size_t cap, size_t* len) {
+    if (!ctx || !blob || !len) return fail(WG_EINVAL, "null argument");
+    if (cap < sizeof(Blob)) return fail(WG_EINVAL, "blob capacity %zu < %zu", cap, sizeof(Blob));
+    Blob b;
+    std::memset(&b, 0, sizeof(b));
+    b.magic = kBlobMagic;
+    b.gpu_index = ctx->cfg.gpu_index;
+    b.P = ctx->cfg.P;
+    b.R = ctx->R;
+    b.D = ctx->D;
+    b.Dv = ctx->Dv;
+    b.dtype = ctx->cfg.dtype;
+    b.n = ctx->cfg.n;
+    b.arena_bytes = ctx->L.total;
+    WG_CUDA(cudaSetDevice(ctx->cfg.device));
+    WG_CUDA(cudaIpcGetMemHandle(&b.handle, ctx->arena));
+    std::memcpy(blob, &b, sizeof(b));
+    *len = sizeof(b);
+    return WG_OK;
+}
+
+int wg_ctx_import_peer(wg_ctx* ctx, int gpu_index, const void* blob, size_t len) {
+    if (!ctx || !blob) return fail(WG_EINVAL, "null argument");
+    if (len != sizeof(Blob)) return fail(WG_EINVAL, "blob length %zu != %zu", len, sizeof(Blob));
+    Blob b;
+    std::memcpy(&b, blob, sizeof(b));
+    if (b.magic != kBlobMagic) return fail(WG_EINVAL, "bad blob magic");
+    if (b.gpu_index != gpu_index || gpu_index < 0 || gpu_index >= ctx->cfg.n_gpus)
+        return fail(WG_EINVAL, "blob is for gpu %d, expected %d", b.gpu_index, gpu_index);
+    if (b.P != ctx->cfg.P || b.R != ctx->R || b.D != ctx->D || b.Dv != ctx->Dv || b.dtype != ctx->cfg.dtype ||
+        b.n != ctx->cfg.n || b.arena_bytes != ctx->L.total)
+        return fail(WG_EINVAL, "peer %d context geometry differs", gpu_index);
+    if (gpu_index == ctx->cfg.gpu_index) return WG_OK;
+    if (ctx->opened[gpu_index]) return WG_OK;
+    WG_CUDA(cudaSetDevice(ctx->cfg.device));
+    void* ptr = nullptr;
+    WG_CUDA(cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess));
+    ctx->base[gpu_index] = static_cast<char*>(ptr);
+    ctx->opened[gpu_index] = true;
+    return WG_OK;
+}
+
+static int local_index(wg_ctx* ctx, int rank) {
+    if (rank < 0 || rank >= ctx->cfg.P || rank / ctx->R != ctx->cfg.gpu_index) return -1;
+    return rank % ctx->R;
+}
+
+int wg_ctx_set_initial_model(wg_ctx* ctx, int rank, const void* w0, void* stream) {
+    if (!ctx) return fail(WG_EINVAL, "null ctx");
+    const int l = local_index(ctx, rank);
+    if (l < 0) return fail(WG_EINVAL, "rank %d is not hosted by gpu %d", rank, ctx->cfg.gpu_index);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    WG_CUDA(cudaSetDevice(ctx->cfg.device));
+    char* slot0 = ctx->arena + ctx->L.ring + (int64_t(l) * ctx->D + 0) * ctx->npad * int64_t(ctx->esize);
+    WG_CUDA(cudaMemsetAsync(slot0, 0, size_t(ctx->npad) * ctx->esize, s));
+    if (ctx->cfg.n > 0) WG_CUDA(cudaMemcpyAsync(slot0, w0, size_t(ctx->cfg.n) * ctx->esize, cudaMemcpyDeviceToDevice, s));
+    int64_t* flags0 = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.flags) + (int64_t(l) * ctx->D + 0) * ctx->n_tiles;
+    fill_i64_kernel<<<64, 256, 0, s>>>(flags0, ctx->n_tiles, -1);
+    int64_t* comp = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.complete) + int64_t(l) * ctx->D + 0;
+    fill_i64_kernel<<<1, 32, 0, s>>>(comp, 1, -1);
+    WG_CUDA(cudaGetLastError());
+    return WG_OK;
+}
+
+int wg_install(wg_ctx* ctx, int rank, int64_t stamp, const void* vec, void* stream) {
+    if (!ctx || (!vec && ctx->cfg.n)) return fail(WG_EINVAL, "null argument");
+    const int l = local_index(ctx, rank);
+    if (l < 0) return fail(WG_EINVAL, "rank %d is not hosted by gpu %d", rank, ctx->cfg.gpu_index);
+    if (stamp < 0) return fail(WG_EINVAL, "install stamp must be >= 0");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    WG_CUDA(cudaSetDevice(ctx->cfg.device));
+    const int slot = int((stamp + 1) % ctx->D);
+    char* dst = ctx->arena + ctx->L.ring + (int64_t(l) * ctx->D + slot) * ctx->npad * int64_t(ctx->esize);
+    if (ctx->cfg.n > 0) WG_CUDA(cudaMemcpyAsync(dst, vec, size_t(ctx->cfg.n) * ctx->esize, cudaMemcpyDeviceToDevice, s));
+    int64_t* flags = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.flags) + (int64_t(l) * ctx->D + slot) * ctx->n_tiles;
+    fill_i64_kernel<<<64, 256, 0, s>>>(flags, ctx->n_tiles, stamp);
+    int64_t* comp = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.complete) + int64_t(l) * ctx->D + slot;
+    fill_i64_kernel<<<1, 32, 0, s>>>(comp, 1, stamp);
+    int64_t* ann = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.announce) + int64_t(l) * kAnnounceStride;
+    fill_i64_kernel<<<1, 32, 0, s>>>(ann, 1, stamp);
+    WG_CUDA(cudaGetLastError());
+    return WG_OK;
+}
+
+int wg_ctx_slot(wg_ctx* ctx, int rank, int64_t stamp, void** ptr, int64_t* held_stamp) {
+    if (!ctx || !ptr) return fail(WG_EINVAL, "null argument");
+    if (rank < 0 || rank >= ctx->cfg.P || stamp < -1) return fail(WG_EINVAL, "rank/stamp out of range");
+    char* b = ctx->base[rank / ctx->R];
+    if (!b) return fail(WG_EINVAL, "gpu %d not imported", rank / ctx->R);
+    const int l = rank % ctx->R;
+    const int slot = int((stamp + 1) % ctx->D);
+    *ptr = b + ctx->L.ring + (int64_t(l) * ctx->D + slot) * ctx->npad * int64_t(ctx->esize);
+    if (held_stamp) {
+        WG_CUDA(cudaSetDevice(ctx->cfg.device));
+        WG_CUDA(cudaMemcpy(held_stamp, b + ctx->L.complete + (int64_t(l) * ctx->D + slot) * 8, 8,
+                           cudaMemcpyDeviceToHost));
+    }
+    return WG_OK;
+}
+
+static int occupancy(wg_ctx* ctx, int n_stage) {
+    if (ctx->occ[n_stage] > 0) return ctx->occ[n_stage];
+    int occ = 0;
+    const size_t smem = size_t(n_stage) * kThreads * kVecPerThread * 16;
+    cudaError_t e = ctx->cfg.dtype == WG_F32
+                        ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wagma_step_kernel<float>, kThreads, smem)
+                        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wagma_step_kernel<double>, kThreads, smem);
+    if (e != cudaSuccess || occ < 1) occ = 1;
+    ctx->occ[n_stage] = occ;
+    return occ;
+}
+
+int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced_versions,
+              const int64_t* forced_stamps, int n_forced, void* stream) {
+    if (!ctx || (!jobs && n_jobs)) return fail(WG_EINVAL, "null argument");
+    const wg_config& c = ctx->cfg;
+    if (n_jobs < 1 || n_jobs > ctx->R) return fail(WG_EINVAL, "n_jobs=%d must be in [1, %d]", n_jobs, ctx->R);
+    if (n_forced < 0 || n_forced > kMaxVersions || (n_forced && (!forced_versions || !forced_stamps)))
+        return fail(WG_EINVAL, "forced stamp table");
+    for (int g = 0; g < c.n_gpus; ++g)
+        if (!ctx->base[g]) return fail(WG_EINVAL, "peer gpu %d not imported", g);
+
+    static thread_local LaunchParams p;
+    std::memset(&p, 0, sizeof(p));
+    for (int g = 0; g < kMaxGpus; ++g) p.base[g] = ctx->base[g];
+    p.L = ctx->L;
+    p.P = c.P;
+    p.S = c.S;
+    p.R = ctx->R;
+    p.G = c.n_gpus;
+    p.gpu_index = c.gpu_index;
+    p.D = ctx->D;
+    p.Dv = ctx->Dv;
+    p.need_fence = c.n_gpus > 1;
+    p.n = c.n;
+    p.npad = ctx->npad;
+    p.n_tiles = ctx->n_tiles;
+    p.tile_elems = ctx->tile_elems;
+    p.grace_ns = c.grace_ns;
+    p.timeout_ns = c.timeout_ns;
+    p.staleness_bound = c.staleness_bound;
+    p.status = ctx->status_dev;
+    for (int q = 0; q < kMaxP; ++q) p.job_of_rank[q] = -1;
+
+    const size_t align_mask = 15;
+    auto misaligned = [&](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & align_mask) != 0; };
+    // jobs and their versions
+    for (int j = 0; j < n_jobs; ++j) {
+        const wg_job& in = jobs[j];
+        const int l = local_index(ctx, in.rank);
+        if (l < 0) return fail(WG_EINVAL, "job %d: rank %d not hosted here", j, in.rank);
+        if (p.job_of_rank[in.rank] >= 0) return fail(WG_EINVAL, "rank %d has two jobs in one launch", in.rank);
+        if (in.kind < WG_JOB_STEP || in.kind > WG_JOB_SYNC_SUM) return fail(WG_EINVAL, "job %d: kind", j);
+        if (in.version < 0) return fail(WG_EINVAL, "job %d: negative version", j);
+        const bool fused = in.kind <= WG_JOB_LOCAL_STEP;
+        if (fused) {
+            if (c.n && (!in.W || !in.g || misaligned(in.W) || misaligned(in.g)))
+                return fail(WG_EINVAL, "job %d: W/g must be 16-byte aligned device pointers", j);
+            if (in.update_rule == WG_UPDATE_MOMENTUM && c.n && (!in.m || misaligned(in.m)))
+                return fail(WG_EINVAL, "job %d: momentum buffer", j);
+            if (in.update_rule != WG_UPDATE_SGD && in.update_rule != WG_UPDATE_MOMENTUM)
+                return fail(WG_EINVAL, "job %d: update rule", j);
+        } else if (c.n && (!in.fresh || !in.acc_out || misaligned(in.fresh) || misaligned(in.acc_out))) {
+            return fail(WG_EINVAL, "job %d: fresh/acc_out must be 16-byte aligned device pointers", j);
+        }
+        DevJob& d = p.jobs[j];
+        d.rank = in.rank;
+        d.local = l;
+        d.kind = in.kind;
+        d.update_rule = in.update_rule;
+        d.version = in.version;
+        d.eta = in.eta;
+        d.beta = in.beta;
+        d.W = in.W;
+        d.m = in.m;
+        d.g = in.g;
+        d.fresh = in.fresh;
+        d.acc_out = in.acc_out;
+        d.produces = in.kind != WG_JOB_LOCAL_STEP;
+        d.plan = -1;
+        d.vidx = -1;
+        p.job_of_rank[in.rank] = j;
+        if (in.kind == WG_JOB_LOCAL_STEP) continue;
+        const bool sync = in.kind == WG_JOB_SYNC_STEP || in.kind == WG_JOB_SYNC_SUM;
+        int vi = -1;
+        for (int k = 0; k < p.n_versions; ++k)
+            if (p.versions[k].version == in.version) vi = k;
+        if (vi < 0) {
+            if (p.n_versions == kMaxVersions) return fail(WG_EINVAL, "too many versions in one launch");
+            vi = p.n_versions++;
+            DevVersion& dv = p.versions[vi];
+            dv.version = in.version;
+            dv.forced_idx = -1;
+            if (sync) {
+                dv.mode = kSync;
+            } else {
+                for (int f = 0; f < n_forced; ++f)
+                    if (forced_versions[f] == in.version) dv.forced_idx = f;
+                dv.mode = dv.forced_idx >= 0 ? kForced : (c.activation_enabled ? kLive : kBlocking);
+            }
+        } else if ((p.versions[vi].mode == kSync) != sync) {
+            return fail(WG_EINVAL, "version %lld mixes sync and group jobs", (long long)in.version);
+        }
+        d.vidx = vi;
+    }
+    for (int f = 0; f < n_forced; ++f)
+        for (int q = 0; q < c.P; ++q) p.forced[f][q] = forced_stamps[int64_t(f) * c.P + q];
+    p.n_jobs = n_jobs;
+
+    // summation plans: one per distinct (version, group)
+    int leaves[kMaxLeaves];
+    for (int j = 0; j < n_jobs; ++j) {
+        DevJob& d = p.jobs[j];
+        if (d.kind == WG_JOB_LOCAL_STEP) continue;
+        const bool sync = d.kind == WG_JOB_SYNC_STEP || d.kind == WG_JOB_SYNC_SUM;
+        int nl = 0;
+        if (sync) {
+            nl = c.P;  // masks 1,2,..,P/2 (collective.py:368): leaf i = rank i
+            for (int i = 0; i < nl; ++i) leaves[i] = i;
+        } else {
+            int grp[kMaxP], ng = 0;
+            int rc = group_of(c.P, c.S, d.version, c.mask_rule, d.rank, grp, &ng);
+            if (rc) return fail(rc, "group_of failed");
+            rc = tree_leaves(c.P, c.S, d.version, c.mask_rule, grp[0], leaves, &nl);
+            if (rc) return fail(rc, "tree_leaves failed");
+            if (p.versions[d.vidx].mode == kBlocking || p.versions[d.vidx].mode == kSync) {
+                // blocking: every local member must join in this launch
+                for (int i = 0; i < ng; ++i) {
+                    const int q = grp[i];
+                    if (q / ctx->R != c.gpu_index) continue;
+                    const int jq = p.job_of_rank[q];
+                    if (jq < 0 || jobs[jq].version != d.version)
+                        return fail(WG_EINVAL, "blocking version %lld: local member %d not in launch",
+                                    (long long)d.version, q);
+                }
+            }
+        }
+        int pl = -1;
+        for (int k = 0; k < p.n_plans && pl < 0; ++k) {
+            const DevPlan& P_ = p.plans[k];
+            if (P_.vidx != d.vidx || P_.n_leaves != nl) continue;
+            bool same = true;
+            for (int i = 0; i < nl && same; ++i) same = P_.leaves[i] == leaves[i];
+            const bool same_kind = (p.jobs[P_.members[0]].kind == WG_JOB_SYNC_STEP ||
+                                    p.jobs[P_.members[0]].kind == WG_JOB_SYNC_SUM) == sync;
+            if (same && same_kind) pl = k;
+        }
+        if (pl < 0) {
+            if (p.n_plans == kMaxPlans) return fail(WG_EINVAL, "too many plans");
+            pl = p.n_plans++;
+            DevPlan& P_ = p.plans[pl];
+            P_.vidx = d.vidx;
+            P_.n_leaves = nl;
+            P_.log_leaves = ilog2(nl);
+            P_.divisor = sync ? c.P : c.S;
+            P_.n_members = 0;
+            for (int i = 0; i < nl; ++i) P_.leaves[i] = int16_t(leaves[i]);
+        }
+        DevPlan& P_ = p.plans[pl];
+        P_.members[P_.n_members++] = int8_t(j);
+        d.plan = pl;
+    }
+    {
+        // sync versions: all local ranks must join in the same launch
+        for (int vi = 0; vi < p.n_versions; ++vi) {
+            if (p.versions[vi].mode != kSync) continue;
+            for (int l = 0; l < ctx->R; ++l) {
+                const int q = c.gpu_index * ctx->R + l;
+                const int jq = p.job_of_rank[q];
+                if (jq < 0 || jobs[jq].version != p.versions[vi].version)
+                    return fail(WG_EINVAL, "sync version %lld: local rank %d not in launch",
+                                (long long)p.versions[vi].version, q);
+            }
+        }
+    }
+
+    int n_stage = 0;
+    for (int j = 0; j < n_jobs; ++j) n_stage = std::max(n_stage, p.jobs[j].produces ? j + 1 : 0);
+    const size_t smem = size_t(std::max(n_stage, 1)) * kThreads * kVecPerThread * 16;
+    const int occ = occupancy(ctx, std::max(n_stage, 1));
+    const int64_t grid = std::min<int64_t>(ctx->n_tiles, int64_t(occ) * ctx->sms);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    WG_CUDA(cudaSetDevice(c.device));
+    if (c.dtype == WG_F32)
+        wagma_step_kernel<float><<<unsigned(grid), kThreads, smem, s>>>(p);
+    else
+        wagma_step_kernel<double><<<unsigned(grid), kThreads, smem, s>>>(p);
+    WG_CUDA(cudaGetLastError());
+    ctx->last_n_jobs = n_jobs;
+    return WG_OK;
+}
+
+int wg_launch_status(wg_ctx* ctx, int i, wg_job_status* out) {
+    if (!ctx || !out) return fail(WG_EINVAL, "null argument");
+    if (i < 0 || i >= ctx->last_n_jobs) return fail(WG_EINVAL, "job index %d out of range", i);
+    std::memcpy(out, const_cast<const wg_job_status*>(ctx->status_host) + i, sizeof(*out));
+    return WG_OK;
+}
+
+int wg_query_version(wg_ctx* ctx, int64_t version, int64_t* stamps, int* locked) {
+    if (!ctx || !stamps || !locked || version < 0) return fail(WG_EINVAL, "bad argument");
+    if (!ctx->base[0]) return fail(WG_EINVAL, "gpu 0 not imported");
+    Desc d;
+    WG_CUDA(cudaSetDevice(ctx->cfg.device));
+    WG_CUDA(cudaMemcpy(&d, ctx->base[0] + ctx->L.desc + (version % ctx->Dv) * int64_t(sizeof(Desc)), sizeof(Desc),
+                       cudaMemcpyDeviceToHost));
+    *locked = d.state == (version + 1) * 4 + 2;
+    for (int q = 0; q < ctx->cfg.P; ++q) stamps[q] = d.stamps[q];
+    return WG_OK;
+}
+
+int wg_ctx_error(wg_ctx* ctx, int* code, int64_t* info) {
+    if (!ctx || !code) return fail(WG_EINVAL, "null argument");
+    int64_t h[2];
+    WG_CUDA(cudaSetDevice(ctx->cfg.device));
+    WG_CUDA(cudaMemcpy(h, ctx->arena + ctx->L.hdr, sizeof(h), cudaMemcpyDeviceToHost));
+    *code = int(h[0]);
+    if (info) *info = h[1];
+    return WG_OK;
+}
+
+int wg_ctx_clear_error(wg_ctx* ctx) {
+    if (!ctx) return fail(WG_EINVAL, "null ctx");
+    WG_CUDA(cudaSetDevice(ctx->cfg.device));
+    WG_CUDA(cudaMemset(ctx->arena + ctx->L.hdr, 0, 16));
+    return WG_OK;
+}
+
+int wg_delay(wg_ctx* ctx, int64_t ns, void* stream) {
+    if (!ctx) return fail(WG_EINVAL, "null ctx");
+    if (ns <= 0) return WG_OK;
+    WG_CUDA(cudaSetDevice(ctx->cfg.device));
+    delay_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(ns);
+    WG_CUDA(cudaGetLastError());
+    return WG_OK;
+}
+
+int wg_ctx_geometry(wg_ctx* ctx, int64_t* tile_elems, int64_t* n_tiles, int* grid, int* ring_depth) {
+    if (!ctx) return fail(WG_EINVAL, "null ctx");
+    if (tile_elems) *tile_elems = ctx->tile_elems;
+    if (n_tiles) *n_tiles = ctx->n_tiles;
+    if (grid) *grid = int(std::min<int64_t>(ctx->n_tiles, int64_t(occupancy(ctx, ctx->R)) * ctx->sms));
+    if (ring_depth) *ring_depth = ctx->D;
+    return WG_OK;
+}
+
+}  // extern "C"

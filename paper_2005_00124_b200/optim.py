@@ -1,0 +1,172 @@
+"""Group model averaging SGD on the device (drop-in for the hot path of `wagma.optim`).
+
+Keeps the reference's configuration surface -- `EtaSchedule`,
+`OptimizerConfig` (with the same validation and errors), `is_sync_iteration`,
+`ConfigError`, `DivergenceError` -- and replaces the per-worker Alg. 2 loop
+(`_GroupAveragingWorker`, optim.py:371-452) by `GroupAveragingOptimizer`,
+whose `step()` issues ONE fused device launch per iteration for all ranks a
+process hosts: local SGD/momentum update, send-buffer install, group (or
+global) allreduce and the averaging rule, touching each weight once.
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass, field
+from typing import Mapping, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .context import DeviceContext, Job, JobStatus
+from .topology import GroupingParams
+
+__all__ = [
+    "EtaSchedule",
+    "OptimizerConfig",
+    "ConfigError",
+    "DivergenceError",
+    "is_sync_iteration",
+    "GroupAveragingOptimizer",
+]
+
+
+class ConfigError(ValueError):
+    """Invalid run configuration (optim.py:77-78)."""
+
+
+class DivergenceError(RuntimeError):
+    """Non-finite gradient or loss encountered during training (optim.py:81-82)."""
+
+
+@dataclass(frozen=True)
+class EtaSchedule:
+    """Learning-rate schedule: constant, step decay, or P/sqrt(T) (optim.py:85-103)."""
+
+    kind: str = "constant"
+    value: float = 0.1
+    decay_factor: float = 0.5
+    decay_every: int = 0
+
+    def rate(self, t: int, P: int, T: int) -> float:
+        if self.kind == "constant":
+            return self.value
+        if self.kind == "step":
+            if self.decay_every <= 0:
+                raise ConfigError("step schedule needs decay_every >= 1")
+            return self.value * self.decay_factor ** (t // self.decay_every)
+        if self.kind == "theorem":
+            return float(P / np.sqrt(T))
+        raise ConfigError(f"unknown eta schedule kind {self.kind!r}")
+
+
+@dataclass
+class OptimizerConfig:
+    """The four averaging parameters plus local-update settings (optim.py:106-148).
+
+    ``tau=None`` means no global synchronization. ``alpha`` selects the
+    wait-avoiding group allreduce, ``beta`` the blocking one; both off
+    degrades to local SGD with period tau.
+    """
+
+    T: int
+    S: int = 1
+    tau: Optional[int] = None
+    alpha: bool = True
+    beta: bool = False
+    eta: EtaSchedule = field(default_factory=EtaSchedule)
+    b: int = 1
+    update_rule: str = "sgd"
+    momentum: float = 0.9
+
+    def validate(self, P: int) -> None:
+        if self.alpha and self.beta:
+            raise ConfigError("alpha and beta can not both be set")
+        if self.T < 1:
+            raise ConfigError("T must be >= 1")
+        if self.tau is not None and self.tau < 1:
+            raise ConfigError("tau must be >= 1 or None")
+        if self.b < 1:
+            raise ConfigError("batch size must be >= 1")
+        if self.update_rule not in ("sgd", "momentum"):
+            raise ConfigError(f"unknown update rule {self.update_rule!r}")
+        try:
+            GroupingParams(P, self.S, 0)
+        except ValueError as exc:
+            raise ConfigError(str(exc)) from exc
+        if self.eta.kind == "constant" and self.eta.value <= 0:
+            raise ConfigError("eta must be positive")
+        if self.eta.kind == "theorem" and self.tau is not None:
+            horizon = P ** 4 * self.tau ** 4
+            if self.T < horizon:
+                warnings.warn(f"theorem schedule expects T >= P^4 tau^4 = {horizon}, got T={self.T}",
+                              stacklevel=2)
+
+
+def is_sync_iteration(t: int, tau: Optional[int]) -> bool:
+    """(optim.py:151-152)"""
+    return tau is not None and (t + 1) % tau == 0
+
+
+class GroupAveragingOptimizer:
+    """Alg. 2 for the ranks of one `DeviceContext`, one fused launch per step.
+
+    Owns the replicas W_r (initialised to ``w0`` on every rank, optim.py:328)
+    and the local momentum buffers m_r (never averaged, optim.py:165/179).
+    ``step(t, grads)`` enqueues iteration t for the given ranks on the
+    current stream: sync iterations run the blocking global average
+    (optim.py:406-411, 449-452), other iterations the wait-avoiding (alpha)
+    or blocking (beta) group average (optim.py:412-447), or a plain local
+    step when both flags are off (optim.py:427-428).
+    """
+
+    def __init__(self, ctx: DeviceContext, cfg: OptimizerConfig, w0: torch.Tensor, *, T: Optional[int] = None):
+        cfg.validate(ctx.P)
+        if cfg.S != ctx.S:
+            raise ConfigError(f"config S={cfg.S} differs from the context's S={ctx.S}")
+        self.use_group = cfg.alpha or cfg.beta
+        if self.use_group and bool(cfg.alpha) != ctx.activation_enabled:
+            raise ConfigError("alpha/beta must match the context's activation_enabled")
+        if cfg.tau != ctx.tau:
+            raise ConfigError(f"config tau={cfg.tau} differs from the context's tau={ctx.tau}")
+        self.ctx = ctx
+        self.cfg = cfg
+        self.T = cfg.T if T is None else T
+        self.momentum = cfg.update_rule == "momentum"
+        w0 = w0.to(device=ctx.torch_device, dtype=ctx.dtype).contiguous()
+        self.W: dict[int, torch.Tensor] = {}
+        self.m: dict[int, Optional[torch.Tensor]] = {}
+        for r in ctx.local_ranks:
+            self.W[r] = w0.clone()
+            self.m[r] = torch.zeros_like(w0) if self.momentum else None
+            ctx.set_initial_model(r, w0)
+
+    def kind(self, t: int) -> int:
+        if is_sync_iteration(t, self.cfg.tau):
+            return _lib.WG_JOB_SYNC_STEP
+        return _lib.WG_JOB_STEP if self.use_group else _lib.WG_JOB_LOCAL_STEP
+
+    def jobs(self, versions: Mapping[int, int], grads: Mapping[int, torch.Tensor]) -> list[Job]:
+        """Jobs for {rank: iteration} with gradients {rank: g}."""
+        out = []
+        for r, t in versions.items():
+            out.append(Job(rank=r, kind=self.kind(t), version=t, W=self.W[r], m=self.m[r], g=grads[r],
+                           eta=self.cfg.eta.rate(t, self.ctx.P, self.T), beta=self.cfg.momentum,
+                           momentum=self.momentum))
+        return out
+
+    def step(self, t: int, grads: Mapping[int, torch.Tensor], *, forced_stamps: Optional[list[int]] = None,
+             stream=None) -> None:
+        """Iteration t for every rank in ``grads`` (all local ranks normally)."""
+        versions = {r: t for r in grads}
+        forced = {t: forced_stamps} if forced_stamps is not None else None
+        self.ctx.launch(self.jobs(versions, grads), forced=forced, stream=stream)
+
+    def step_mixed(self, versions: Mapping[int, int], grads: Mapping[int, torch.Tensor],
+                   forced: Optional[dict[int, list[int]]] = None, stream=None) -> None:
+        """One launch in which ranks may be at different iterations (stragglers)."""
+        self.ctx.launch(self.jobs(versions, grads), forced=forced, stream=stream)
+
+    def statuses(self) -> list[JobStatus]:
+        return self.ctx.statuses()

@@ -1,0 +1,63 @@
+"""Deterministic straggler schedule (drop-in for `wagma.netsim.StragglerPolicy`/`DelayModel`).
+
+The reference injects load imbalance by picking victims per iteration with
+numpy's PCG64 (`StragglerPolicy.victims`, netsim.py:75-82) and adding a
+fixed extra delay (`compute_delay`, netsim.py:103-117). The victim choice is
+reproduced with the very same numpy call, so the schedule is bit-identical;
+the delay itself becomes a device-side spin on the victim's stream
+(`DeviceContext.delay`), so no host sleep sits inside a timed region.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+__all__ = ["StragglerPolicy", "DelayModel", "compute_delay"]
+
+
+@dataclass(frozen=True)
+class StragglerPolicy:
+    """Per-iteration delay injection: pick victims, add a fixed extra delay."""
+
+    victims_per_iteration: int
+    extra_delay_ms: float
+    selection_seed: int = 0
+
+    def victims(self, iteration: int, P: int) -> frozenset[int]:
+        if self.victims_per_iteration <= 0:
+            return frozenset()
+        if self.victims_per_iteration > P:
+            raise ValueError("victims_per_iteration exceeds process count")
+        rng = np.random.default_rng([self.selection_seed, iteration])
+        picks = rng.choice(P, size=self.victims_per_iteration, replace=False)
+        return frozenset(int(v) for v in picks)
+
+
+@dataclass(frozen=True)
+class DelayModel:
+    """Compute timing of one run (netsim.py:85-100); delays in ms, >= 0."""
+
+    base_compute_ms: float = 1.0
+    jitter_max_ms: float = 0.0
+    link_latency_ms: float = 1.0
+    straggler: Optional[StragglerPolicy] = None
+
+    def __post_init__(self) -> None:
+        if min(self.base_compute_ms, self.jitter_max_ms, self.link_latency_ms) < 0:
+            raise ValueError("delays must be non-negative")
+
+
+def compute_delay(proc: int, iteration: int, model: DelayModel, rng_seed: int, P: int) -> float:
+    """base + uniform jitter + extra if victim (netsim.py:103-117), in ms."""
+    if not 0 <= proc < P:
+        raise ValueError(f"rank {proc} out of range for P={P}")
+    delay = model.base_compute_ms
+    if model.jitter_max_ms > 0:
+        rng = np.random.default_rng([rng_seed, iteration, proc])
+        delay += float(rng.uniform(0.0, model.jitter_max_ms))
+    if model.straggler is not None and proc in model.straggler.victims(iteration, P):
+        delay += model.straggler.extra_delay_ms
+    return delay
