@@ -1,0 +1,401 @@
+"""WAGMA group-averaging benchmark (BASELINE.json metric) -- one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N --steps K --warmup W
+
+Workload (BASELINE.json configs[1]): ResNet-50-sized replicas, N = 25,559,081
+fp32 parameters, P = 8 WAGMA ranks, group size S = 8 (north-star target),
+tau = 10, momentum SGD (eta 0.1, beta 0.9), wait-avoiding activation. The P
+ranks are mapped block-wise onto the N GPUs (rank r on GPU r // (P/N)), so
+total work is fixed as N grows ("scaling": "strong"). A step is one WAGMA
+iteration of all P ranks = one fused kernel launch per GPU (local momentum
+step + send-ring install + group / global average). Synthetic data: W0 ~
+N(0, 0.02^2) identical on every rank, g ~ N(0, 0.01^2) (two pre-generated
+gradient buffers per rank, alternated), inputs resident in HBM.
+
+`--impl reference` times the reference path's CPU implementation on the host
+cores: the C restatement of the reference arithmetic in oracle/ (the
+reference itself is Python and does not exist on the GPU box), on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "WAGMA iters/s and group-avg GB/s vs NVLink roofline at 1/2/4/8 B200"
+N_RESNET50 = 25_559_081
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--P", type=int, default=8)
+    ap.add_argument("--S", type=int, default=8)
+    ap.add_argument("--n", type=int, default=N_RESNET50)
+    ap.add_argument("--tau", type=int, default=10)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps (capped at 60)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--grace-us", type=float, default=100.0)
+    return ap.parse_args()
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fp:
+            d = json.load(fp)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def workload_name(a):
+    model = "ResNet-50-sized" if a.n == N_RESNET50 else f"n={a.n}"
+    return f"{model} WAGMA group averaging, P={a.P} ranks, S={a.S}, tau={a.tau}, momentum"
+
+
+def config_dict(a, G):
+    return {"workload": workload_name(a), "params_per_replica": a.n, "ranks": a.P, "group_size": a.S,
+            "tau": a.tau, "update_rule": "momentum", "eta": 0.1, "beta": 0.9, "activation": "wait-avoiding",
+            "rank_mapping": f"block ({a.P // G} ranks per GPU)", "parallelism": f"wagma-p{a.P}-g{G}",
+            "l2": "inputs larger than L2 (every step streams all replicas, > 1 GB)"}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle's C restatement of the reference arithmetic
+# ---------------------------------------------------------------------------
+
+def cpu_port_run(a, steps: int, warmup: int, seconds: float):
+    """Time the C port (OpenMP, all host threads) on the same workload.
+
+    Returns (iters_per_s, threads, sample_description, per_iter_s)."""
+    from oracle import c_oracle
+    from oracle import topology_oracle as otopo
+    dt = np.float32 if a.dtype == "f32" else np.float64
+    P, n = a.P, a.n
+    rng = np.random.default_rng(1234)
+    w0 = (rng.standard_normal(n) * 0.02).astype(dt)
+    W = [w0.copy() for _ in range(P)]
+    m = [np.zeros(n, dt) for _ in range(P)]
+    g = [(rng.standard_normal(n) * 0.01).astype(dt) for _ in range(P)]
+    wp = [np.empty(n, dt) for _ in range(P)]
+    threads = c_oracle.max_threads()
+
+    def one(t):
+        sync = (t + 1) % a.tau == 0
+        masks = [1 << j for j in range(P.bit_length() - 1)] if sync else list(otopo.phase_masks(P, a.S, t))
+        c_oracle.wagma_iteration(W, m, g, wp, masks, P if sync else a.S, 0.1, 0.9, True, nthreads=threads)
+
+    for t in range(warmup):
+        one(t)
+    times = []
+    t0 = time.perf_counter()
+    t = warmup
+    while len(times) < steps:
+        s = time.perf_counter()
+        one(t)
+        times.append(time.perf_counter() - s)
+        t += 1
+        if seconds and time.perf_counter() - t0 > seconds and len(times) >= 2:
+            break
+    total = sum(times)
+    sample = (f"{len(times)} iterations of P={P} ranks x N={n} {a.dtype} (local step + S={a.S} group sums "
+              f"in the reference's recursive-doubling order + averaging), C/OpenMP port of the reference "
+              f"arithmetic, {threads} threads")
+    return len(times) / total, threads, sample, total / len(times)
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ips, threads, sample, _ = cpu_port_run(a, a.steps, a.warmup, seconds=a.cpu_seconds * 3)
+    line = {"metric": METRIC, "value": ips, "unit": "iters/s", "impl": "reference", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 / ips, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
+            "config": config_dict(a, max(1, a.gpus)),
+            "cpu_baseline": {"value": ips, "unit": "iters/s", "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": ips, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as fp:
+            for line in fp:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes
+# ---------------------------------------------------------------------------
+
+def step_bytes(a, G, gpu_index, t, elem):
+    """(HBM bytes, NVLink ingress bytes) one launch on `gpu_index` must move.
+
+    Own streams per local rank: read W, m, g; write m, the send-slot W' and
+    W_{t+1} = 6 * elem * n. Each leaf of a group sum living on another GPU
+    crosses NVLink once (ingress here) and is read from the owner's HBM (by
+    symmetry the same count is served from this GPU's HBM).
+    """
+    from paper_2005_00124_b200.topology import GroupingParams, compute_groups, tree_leaves
+    R = a.P // G
+    local = range(gpu_index * R, (gpu_index + 1) * R)
+    own = R * 6 * elem * a.n
+    sync = (t + 1) % a.tau == 0
+    remote_leaves = 0
+    if sync:
+        remote_leaves = a.P - R  # one global plan per GPU
+    else:
+        part = compute_groups(GroupingParams(a.P, a.S, t))
+        seen = set()
+        for r in local:
+            grp = part.group_of(r)
+            if grp in seen:
+                continue
+            seen.add(grp)
+            leaves = tree_leaves(GroupingParams(a.P, a.S, t), grp[0])
+            remote_leaves += sum(1 for q in leaves if q // R != gpu_index)
+    nvl = remote_leaves * elem * a.n
+    return own + nvl, nvl
+
+
+def load_traffic(a, G):
+    """dram bytes per launch from a committed ncu --set full capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fp:
+        d = json.load(fp)
+    key = f"P{a.P}_S{a.S}_n{a.n}_{a.dtype}_g{G}"
+    v = d.get(key)
+    return v.get("dram_bytes_per_launch") if isinstance(v, dict) else None
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_00124_b200.context import DeviceContext
+    from paper_2005_00124_b200.optim import EtaSchedule, GroupAveragingOptimizer, OptimizerConfig
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    G = world
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dt = torch.float32 if a.dtype == "f32" else torch.float64
+    elem = 4 if a.dtype == "f32" else 8
+    if a.P % G:
+        raise SystemExit(f"P={a.P} must be divisible by the GPU count {G}")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ctx = DeviceContext(a.P, a.S, a.n, dtype=dt, tau=a.tau, n_gpus=G, gpu_index=rank, device=dev.index,
+                        grace_us=a.grace_us, timeout_s=30.0)
+    cfg = OptimizerConfig(T=1 << 30, S=a.S, tau=a.tau, alpha=True, eta=EtaSchedule(value=0.1),
+                          update_rule="momentum", momentum=0.9)
+    gen = torch.Generator(device=dev).manual_seed(1234)
+    w0 = torch.randn(a.n, generator=gen, device=dev, dtype=dt) * 0.02
+    opt = GroupAveragingOptimizer(ctx, cfg, w0)
+    local = list(ctx.local_ranks)
+    gpool = {r: [torch.randn(a.n, generator=gen, device=dev, dtype=dt) * 0.01 for _ in range(2)] for r in local}
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+    barrier()
+
+    t = 0
+    for _ in range(a.warmup):
+        opt.step(t, {r: gpool[r][t % 2] for r in local})
+        t += 1
+    sampler = ClockSampler(dev.index) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = ctx.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_first = t
+    start.record(stream)
+    for k in range(a.steps):
+        ev[k][0].record(stream)
+        opt.step(t, {r: gpool[r][t % 2] for r in local})
+        ev[k][1].record(stream)
+        t += 1
+    end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    gpu_launches = ctx.launches - launches0
+    ctx.check()
+    elapsed_ms = allmax(start.elapsed_time(end))
+    kern_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(a.steps)]
+    kern_avg_ms = allmax(sum(kern_ms) / len(kern_ms))
+    ms_per_step = elapsed_ms / a.steps
+    iters_per_s = 1000.0 * a.steps / elapsed_ms
+
+    # algorithmic bytes of the dominant (only) kernel, averaged over the timed steps
+    hbm_b, nvl_b = 0, 0
+    for tt in range(t_first, t_first + a.steps):
+        h, v = step_bytes(a, G, rank, tt, elem)
+        hbm_b += h
+        nvl_b += v
+    hbm_b /= a.steps
+    nvl_b /= a.steps
+    hbm_peak, peak_kind = measured_peaks()
+    t_hbm = hbm_b / (hbm_peak * 1e9)
+    t_nvl = nvl_b / (NVLINK_PEER_GBS * 1e9)
+    kern_s = kern_avg_ms / 1e3
+    if t_nvl > t_hbm:
+        roof = {"bound": "nvlink", "achieved": nvl_b / kern_s / 1e9, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md; 900 nominal)"}
+    else:
+        roof = {"bound": "hbm", "achieved": hbm_b / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "peak_source": f"{peak_kind} HBM copy (MEASURED_PEAKS.json)"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = load_traffic(a, G)
+    roof["algorithmic_bytes_per_launch"] = {"hbm": hbm_b, "nvlink_ingress": nvl_b}
+    roof["kernel_ms"] = kern_avg_ms
+    roof["roofline_ms"] = max(t_hbm, t_nvl) * 1e3
+    group_avg_gbs = nvl_b / kern_s / 1e9 if nvl_b else 0.0
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not a.no_e2e:
+        ke = a.e2e_steps or min(a.steps, 60)
+        ghost = {r: [gp.cpu().pin_memory() for gp in gpool[r]] for r in local}
+        whost = {r: torch.empty(a.n, dtype=dt).pin_memory() for r in local}
+        gdev = {r: torch.empty(a.n, dtype=dt, device=dev) for r in local}
+        torch.cuda.synchronize()
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(ke):
+            for r in local:
+                gdev[r].copy_(ghost[r][t % 2], non_blocking=True)
+            opt.step(t, gdev)
+            for r in local:
+                whost[r].copy_(opt.W[r], non_blocking=True)
+            t += 1
+        s1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = allmax(s0.elapsed_time(s1))
+        e2e = {"value": 1000.0 * ke / e2e_ms, "unit": "iters/s", "h2d_bytes_per_step": len(local) * elem * a.n,
+               "d2h_bytes_per_step": len(local) * elem * a.n, "steps": ke,
+               "path": "pinned host gradients -> GroupAveragingOptimizer.step -> pinned host replicas"}
+        ctx.check()
+
+    # sanity: replicas finite
+    for r in local:
+        if not torch.isfinite(opt.W[r]).all():
+            raise SystemExit(f"non-finite replica on rank {r}")
+
+    cpu = None
+    if rank == 0 and G == 1 and not a.no_cpu:
+        ips, threads, sample, _ = cpu_port_run(a, 1000, 1, seconds=a.cpu_seconds)
+        cpu = {"value": ips, "unit": "iters/s", "cores": threads, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": iters_per_s, "unit": "iters/s", "n_gpus": G, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": a.dtype, "data": "synthetic", "config": config_dict(a, G),
+                "group_avg_gbs": group_avg_gbs, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": gpu_launches, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -102,7 +102,7 @@ struct DevVersion {
 };
 
 struct DevPlan {
-    int32_t vidx, n_leaves, log_leaves, divisor, n_members, pad;
+    int32_t vidx, n_leaves, log_leaves, divisor, n_members, divisor_pow2;
     int16_t leaves[kMaxLeaves];
     int8_t members[kMaxJobs];
 };
@@ -200,22 +200,22 @@ __device__ __forceinline__ double2 vdiv(double2 a, double d) {
 
 // Caller-owned vectors (W, m, g, fresh, acc_out) have exactly n elements:
 // full 16-byte vectors inside, element-wise handling of the ragged end.
-template <typename T>
+template <typename T, bool FULL = false>
 __device__ __forceinline__ typename Tr<T>::V ld_stream(const T* base, int64_t idx, int64_t n) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
-    if (idx + E <= n) return __ldcs(reinterpret_cast<const V*>(base + idx));
+    if (FULL || idx + E <= n) return __ldcs(reinterpret_cast<const V*>(base + idx));
     V v;
     T* e = reinterpret_cast<T*>(&v);
 #pragma unroll
     for (int i = 0; i < E; ++i) e[i] = (idx + i < n) ? base[idx + i] : T(0);
     return v;
 }
-template <typename T>
+template <typename T, bool FULL = false>
 __device__ __forceinline__ void st_stream(T* base, int64_t idx, int64_t n, typename Tr<T>::V v) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
-    if (idx + E <= n) {
+    if (FULL || idx + E <= n) {
         __stcs(reinterpret_cast<V*>(base + idx), v);
         return;
     }
@@ -459,6 +459,33 @@ __device__ bool resolve_sources(const LaunchParams& p, SmemCtl& sm) {
 // produce: local step, send-ring install, shared-memory stage
 // ---------------------------------------------------------------------------
 
+// Loads of one job's inputs for this thread's vectors of a tile.
+template <typename T>
+__device__ __forceinline__ void load_job(const LaunchParams& p, const DevJob& jb, int64_t tbase,
+                                         typename Tr<T>::V* a, typename Tr<T>::V* b, typename Tr<T>::V* c) {
+    constexpr int E = Tr<T>::EPV;
+    const int tid = threadIdx.x;
+    if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
+        const T* fr = static_cast<const T*>(jb.fresh);
+#pragma unroll
+        for (int k = 0; k < kVecPerThread; ++k) a[k] = ld_stream<T>(fr, tbase + int64_t(k * kThreads + tid) * E, p.n);
+        return;
+    }
+    const T* W = static_cast<const T*>(jb.W);
+    const T* g = static_cast<const T*>(jb.g);
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+        const int64_t idx = tbase + int64_t(k * kThreads + tid) * E;
+        a[k] = ld_stream<T>(W, idx, p.n);
+        b[k] = ld_stream<T>(g, idx, p.n);
+    }
+    if (jb.update_rule == WG_UPDATE_MOMENTUM) {
+        const T* m = static_cast<const T*>(jb.m);
+#pragma unroll
+        for (int k = 0; k < kVecPerThread; ++k) c[k] = ld_stream<T>(m, tbase + int64_t(k * kThreads + tid) * E, p.n);
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void produce_tile(const LaunchParams& p, int64_t tile, typename Tr<T>::V* stage) {
     using V = typename Tr<T>::V;
@@ -466,78 +493,89 @@ __device__ __forceinline__ void produce_tile(const LaunchParams& p, int64_t tile
     constexpr int U = kVecPerThread;
     const int tid = threadIdx.x;
     const int64_t tbase = tile * p.tile_elems;
+    // software pipeline: the next job's loads are in flight while this one
+    // is computed and stored
+    V cw[U], cg[U], cm[U];
+    load_job<T>(p, p.jobs[0], tbase, cw, cg, cm);
     for (int j = 0; j < p.n_jobs; ++j) {
         const DevJob& jb = p.jobs[j];
+        V nw[U], ng[U], nm[U];
+        if (j + 1 < p.n_jobs) load_job<T>(p, p.jobs[j + 1], tbase, nw, ng, nm);
         V wp[U];
         if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
-            const T* fr = static_cast<const T*>(jb.fresh);
 #pragma unroll
-            for (int k = 0; k < U; ++k) wp[k] = ld_stream<T>(fr, tbase + int64_t(k * kThreads + tid) * E, p.n);
+            for (int k = 0; k < U; ++k) wp[k] = cw[k];
         } else {
-            T* W = static_cast<T*>(jb.W);
-            const T* g = static_cast<const T*>(jb.g);
             const T eta = T(jb.eta);
-            V w[U], gv[U];
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                const int64_t idx = tbase + int64_t(k * kThreads + tid) * E;
-                w[k] = ld_stream<T>(W, idx, p.n);
-                gv[k] = ld_stream<T>(g, idx, p.n);
-            }
             if (jb.update_rule == WG_UPDATE_MOMENTUM) {
                 // m = beta*m + g ; W' = W - eta*m  (optim.py:179,183)
                 T* m = static_cast<T*>(jb.m);
                 const T beta = T(jb.beta);
-                V mv[U];
-#pragma unroll
-                for (int k = 0; k < U; ++k) mv[k] = ld_stream<T>(m, tbase + int64_t(k * kThreads + tid) * E, p.n);
 #pragma unroll
                 for (int k = 0; k < U; ++k) {
-                    const V mn = vadd(vscale(beta, mv[k]), gv[k]);
+                    const V mn = vadd(vscale(beta, cm[k]), cg[k]);
                     st_stream<T>(m, tbase + int64_t(k * kThreads + tid) * E, p.n, mn);
-                    wp[k] = vsub(w[k], vscale(eta, mn));
+                    wp[k] = vsub(cw[k], vscale(eta, mn));
                 }
             } else {
                 // W' = W - eta*g  (optim.py:181-183)
 #pragma unroll
-                for (int k = 0; k < U; ++k) wp[k] = vsub(w[k], vscale(eta, gv[k]));
+                for (int k = 0; k < U; ++k) wp[k] = vsub(cw[k], vscale(eta, cg[k]));
             }
             if (jb.kind == WG_JOB_LOCAL_STEP) {
+                T* W = static_cast<T*>(jb.W);
 #pragma unroll
                 for (int k = 0; k < U; ++k) st_stream<T>(W, tbase + int64_t(k * kThreads + tid) * E, p.n, wp[k]);
-                continue;
             }
         }
-        // SendBuffer.install (collective.py:95-101): one write into the ring
-        T* slot = ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + tbase;
+        if (jb.produces) {
+            // SendBuffer.install (collective.py:95-101): one write into the ring
+            T* slot = ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + tbase;
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                __stcg(reinterpret_cast<V*>(slot + int64_t(k * kThreads + tid) * E), wp[k]);
+                stage[(j * U + k) * kThreads + tid] = wp[k];  // thread-private stage
+            }
+        }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
-            __stcg(reinterpret_cast<V*>(slot + int64_t(k * kThreads + tid) * E), wp[k]);
-            stage[(j * U + k) * kThreads + tid] = wp[k];
+            cw[k] = nw[k];
+            cg[k] = ng[k];
+            cm[k] = nm[k];
         }
     }
 }
 
+// Per-tile readiness flags, only read by kernels on OTHER GPUs (ranks on
+// this GPU either read the shared-memory stage of this launch or a slot
+// completed by an earlier launch): a CTA barrier, one system-scope fence and
+// one store per produced slot tile.
 __device__ __forceinline__ void publish_tile(const LaunchParams& p, int64_t tile) {
+    if (!p.need_fence) return;
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (p.need_fence) fence_sys();  // CTA's tile stores visible to peers first
+        fence_sys();
         for (int j = 0; j < p.n_jobs; ++j) {
             const DevJob& jb = p.jobs[j];
-            if (!jb.produces) continue;
-            const int slot = slot_of(p, jb.version);
-            st_relaxed_sys(flag_ptr(p, jb.rank, slot, tile), jb.version);
+            if (jb.produces) st_relaxed_sys(flag_ptr(p, jb.rank, slot_of(p, jb.version), tile), jb.version);
         }
-        for (int j = 0; j < p.n_jobs; ++j) {
-            const DevJob& jb = p.jobs[j];
-            if (!jb.produces) continue;
-            const int slot = slot_of(p, jb.version);
-            unsigned* c = counter_ptr(p, jb.rank, slot);
-            if (atomicAdd(c, 1u) == unsigned(p.n_tiles - 1)) {
-                *c = 0u;  // last tile of this stamp: whole slot published
-                fence_sys();
-                st_release_sys(complete_ptr(p, jb.rank, slot), jb.version);
-            }
+    }
+}
+
+// After the tile loop: add this CTA's tile count to each produced slot's
+// counter; the CTA completing the count publishes the whole slot (`complete`).
+__device__ __forceinline__ void publish_slots(const LaunchParams& p, unsigned my_tiles) {
+    __syncthreads();
+    const int j = threadIdx.x;
+    if (j < p.n_jobs && p.jobs[j].produces && my_tiles) {
+        const DevJob& jb = p.jobs[j];
+        const int slot = slot_of(p, jb.version);
+        fence_sys();
+        unsigned* c = counter_ptr(p, jb.rank, slot);
+        if (atomicAdd(c, my_tiles) + my_tiles == unsigned(p.n_tiles)) {
+            *c = 0u;
+            fence_sys();
+            st_release_sys(complete_ptr(p, jb.rank, slot), jb.version);
         }
     }
 }
@@ -580,6 +618,44 @@ struct TreeSum<T, 0> {
     }
 };
 
+// Trees of 16..64 leaves: 8-leaf subtrees combined through a 4-level
+// register stack (static indices only), same pairing as the full tree.
+template <typename T>
+__device__ __noinline__ void tree_sum_big(const SmemCtl& sm, int pl, int log_leaves, int64_t toff,
+                                          const typename Tr<T>::V* stage, typename Tr<T>::V* out) {
+    using V = typename Tr<T>::V;
+    constexpr int U = kVecPerThread;
+    V s0[U], s1[U], s2[U], s3[U];
+    const int nchunks = 1 << (log_leaves - 3);
+    for (int c = 0; c < nchunks; ++c) {
+        V cur[U];
+        TreeSum<T, 3>::run(sm, pl, c * 8, toff, stage, cur);
+        if (!(c & 1)) {
+#pragma unroll
+            for (int k = 0; k < U; ++k) s0[k] = cur[k];
+            continue;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) cur[k] = vadd(s0[k], cur[k]);
+        if (!(c & 2)) {
+#pragma unroll
+            for (int k = 0; k < U; ++k) s1[k] = cur[k];
+            continue;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) cur[k] = vadd(s1[k], cur[k]);
+        if (!(c & 4)) {
+#pragma unroll
+            for (int k = 0; k < U; ++k) s2[k] = cur[k];
+            continue;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) s3[k] = vadd(s2[k], cur[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) out[k] = log_leaves == 4 ? s1[k] : (log_leaves == 5 ? s2[k] : s3[k]);
+}
+
 template <typename T>
 __device__ __forceinline__ void tree_sum(const SmemCtl& sm, int pl, int log_leaves, int64_t toff,
                                          const typename Tr<T>::V* stage, typename Tr<T>::V* out) {
@@ -588,9 +664,7 @@ __device__ __forceinline__ void tree_sum(const SmemCtl& sm, int pl, int log_leav
         case 1: TreeSum<T, 1>::run(sm, pl, 0, toff, stage, out); break;
         case 2: TreeSum<T, 2>::run(sm, pl, 0, toff, stage, out); break;
         case 3: TreeSum<T, 3>::run(sm, pl, 0, toff, stage, out); break;
-        case 4: TreeSum<T, 4>::run(sm, pl, 0, toff, stage, out); break;
-        case 5: TreeSum<T, 5>::run(sm, pl, 0, toff, stage, out); break;
-        default: TreeSum<T, 6>::run(sm, pl, 0, toff, stage, out); break;
+        default: tree_sum_big<T>(sm, pl, log_leaves, toff, stage, out); break;
     }
 }
 
@@ -619,6 +693,12 @@ __device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, c
         }
         V acc[U];
         tree_sum<T>(sm, pl, P_.log_leaves, tbase, stage, acc);
+        // timely members share one result: acc/S or total/P (optim.py:442,452);
+        // a power-of-two divisor is an exact reciprocal multiply (same IEEE result)
+        V avg[U];
+        const T inv = T(1) / T(P_.divisor);
+#pragma unroll
+        for (int k = 0; k < U; ++k) avg[k] = P_.divisor_pow2 ? vscale(inv, acc[k]) : vdiv(acc[k], T(P_.divisor));
         for (int mi = 0; mi < P_.n_members; ++mi) {
             const int j = P_.members[mi];
             const DevJob& jb = p.jobs[j];
@@ -632,13 +712,9 @@ __device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, c
             const bool timely = jb.kind == WG_JOB_SYNC_STEP || sm.stamps[jb.vidx][jb.rank] == jb.version;
 #pragma unroll
             for (int k = 0; k < U; ++k) {
-                V out;
-                if (timely) {
-                    out = vdiv(acc[k], T(P_.divisor));  // acc/S, total/P (optim.py:442,452)
-                } else {
-                    // late member: (acc + W')/(S+1)  (optim.py:443-444)
-                    out = vdiv(vadd(acc[k], stage[(j * U + k) * kThreads + tid]), T(P_.divisor + 1));
-                }
+                // late member: (acc + W')/(S+1)  (optim.py:443-444), true IEEE division
+                const V out = timely ? avg[k] : vdiv(vadd(acc[k], stage[(j * U + k) * kThreads + tid]),
+                                                     T(P_.divisor + 1));
                 st_stream<T>(W, tbase + int64_t(k * kThreads + tid) * E, p.n, out);
             }
         }
@@ -651,7 +727,7 @@ __device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, c
 // ---------------------------------------------------------------------------
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 2) wagma_step_kernel(const __grid_constant__ LaunchParams p) {
+__global__ void __launch_bounds__(kThreads, 3) wagma_step_kernel(const __grid_constant__ LaunchParams p) {
     using V = typename Tr<T>::V;
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     V* stage = reinterpret_cast<V*>(dyn_smem);
@@ -664,15 +740,18 @@ __global__ void __launch_bounds__(kThreads, 2) wagma_step_kernel(const __grid_co
         __syncthreads();
     }
     bool resolved = false;
+    unsigned my_tiles = 0;
     for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
         produce_tile<T>(p, tile, stage);
         publish_tile(p, tile);
+        ++my_tiles;
         if (!resolved) {
             if (!resolve_sources<T>(p, sm)) break;
             resolved = true;
         }
         if (!consume_tile<T>(p, sm, tile, stage)) break;
     }
+    publish_slots(p, sm.abort ? 0u : my_tiles);
     if (blockIdx.x == 0) {
         if (!resolved && !sm.abort) resolved = resolve_sources<T>(p, sm);
         __syncthreads();
@@ -1112,6 +1191,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
             P_.n_leaves = nl;
             P_.log_leaves = ilog2(nl);
             P_.divisor = sync ? c.P : c.S;
+            P_.divisor_pow2 = is_pow2(P_.divisor);
             P_.n_members = 0;
             for (int i = 0; i < nl; ++i) P_.leaves[i] = int16_t(leaves[i]);
         }

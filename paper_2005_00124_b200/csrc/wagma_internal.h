@@ -12,7 +12,7 @@ constexpr int kMaxVersions = 16;    // distinct versions per launch
 constexpr int kMaxPlans = 16;       // distinct (version, group) sums per launch
 constexpr int kMaxLeaves = 64;      // leaves of one summation tree (sync at P = 64)
 constexpr int kThreads = 256;       // threads per CTA
-constexpr int kVecPerThread = 2;    // 16-byte vectors per thread per tile
+constexpr int kVecPerThread = 1;    // 16-byte vectors per thread per tile
 
 int check_params(int P, int S, int64_t t);
 int phase_masks(int P, int S, int64_t t, int rule, int* masks, int* n_masks);
