@@ -184,6 +184,11 @@ int wg_ctx_clear_error(wg_ctx* ctx);
  * a device-side spin of `ns` nanoseconds on `stream`. */
 int wg_delay(wg_ctx* ctx, int64_t ns, void* stream);
 
+/* Instrumentation: per-CTA phase cycle counters (long long [grid][8]:
+ * produce, publish, resolve, poll, consume, tiles) written by every
+ * multi-GPU launch while dev_buf is non-NULL. */
+int wg_ctx_set_profile(wg_ctx* ctx, void* dev_buf);
+
 /* Number of element tiles and the tile size used by the kernels. */
 int wg_ctx_geometry(wg_ctx* ctx, int64_t* tile_elems, int64_t* n_tiles, int* grid, int* ring_depth);
 

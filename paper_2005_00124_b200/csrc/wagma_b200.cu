@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -74,12 +75,13 @@ struct Layout {
     int64_t complete;  // int64 [R][D]: stamp whose tiles are all published
     int64_t counter;   // uint32 [R][D]: tiles published for the current stamp
     int64_t desc;      // Desc [Dv]  (used on GPU 0 only)
-    int64_t flags;     // int64 [R][D][n_tiles]: stamp held by each slot tile
+    int64_t flags;     // int64 [R][n_tiles][warps]: latest stamp published per warp-tile
     int64_t ring;      // T [R][D][npad]: send ring
     int64_t total;
 };
 
 constexpr int kAnnounceStride = 16;  // int64 words (128 B)
+constexpr int kWarps = kThreads / 32;
 constexpr int64_t kNever = INT64_MIN / 2;
 
 enum VersionMode : int32_t { kLive = 0, kForced = 1, kBlocking = 2, kSync = 3 };
@@ -119,6 +121,9 @@ struct LaunchParams {
     DevPlan plans[kMaxPlans];
     int64_t forced[kMaxVersions][kMaxP];
     wg_job_status* status;
+    long long* prof;  // optional per-CTA phase cycle counters [grid][8]
+    int32_t fence_scope;  // 0 sys (default), 1 gpu, 2 none (timing experiments only)
+    int32_t pad2;
 };
 
 // ---------------------------------------------------------------------------
@@ -242,9 +247,11 @@ __device__ __forceinline__ int64_t* complete_ptr(const LaunchParams& p, int rank
 __device__ __forceinline__ unsigned* counter_ptr(const LaunchParams& p, int rank, int slot) {
     return reinterpret_cast<unsigned*>(rank_base(p, rank) + p.L.counter) + (rank % p.R) * p.D + slot;
 }
-__device__ __forceinline__ int64_t* flag_ptr(const LaunchParams& p, int rank, int slot, int64_t tile) {
+// Readiness flag of one warp's part of a tile: the latest stamp whose W'
+// is written there (monotone per rank; older stamps live in other slots).
+__device__ __forceinline__ int64_t* flag_ptr(const LaunchParams& p, int rank, int64_t tile, int warp) {
     return reinterpret_cast<int64_t*>(rank_base(p, rank) + p.L.flags) +
-           ((int64_t(rank % p.R) * p.D + slot) * p.n_tiles + tile);
+           ((int64_t(rank % p.R) * p.n_tiles + tile) * kWarps + warp);
 }
 template <typename T>
 __device__ __forceinline__ T* ring_ptr(const LaunchParams& p, int rank, int slot) {
@@ -282,6 +289,22 @@ __device__ int spin_eq(const LaunchParams& p, const int64_t* addr, int64_t want,
         v = ld_acquire_sys(addr);
     }
     return 0;
+}
+
+// Spin until *addr >= want (monotone readiness flag). WG_EPROTO if it moved
+// `ring` or more stamps past (the slot holding `want` was overwritten).
+__device__ int spin_geq(const LaunchParams& p, const int64_t* addr, int64_t want, uint64_t t0) {
+    int64_t v = ld_acquire_sys(addr);
+    int it = 0;
+    while (v < want) {
+        if ((++it & 63) == 0) {
+            if (globaltimer() - t0 > uint64_t(p.timeout_ns)) return WG_ETIMEOUT;
+            if (aborted(p)) return WG_ETIMEOUT;
+        }
+        __nanosleep(32);
+        v = ld_acquire_sys(addr);
+    }
+    return v >= want + p.D ? WG_EPROTO : 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -546,18 +569,25 @@ __device__ __forceinline__ void produce_tile(const LaunchParams& p, int64_t tile
     }
 }
 
-// Per-tile readiness flags, only read by kernels on OTHER GPUs (ranks on
-// this GPU either read the shared-memory stage of this launch or a slot
-// completed by an earlier launch): a CTA barrier, one system-scope fence and
-// one store per produced slot tile.
+// Per-warp-tile readiness flags, only read by kernels on OTHER GPUs (ranks on
+// this GPU either read this launch's shared-memory stage or a slot completed
+// by an earlier launch). No CTA barrier: the warp's stores are ordered before
+// lane 0's fence by __syncwarp, the fence before the flag store. Peer loads
+// of this GPU's memory are served by this GPU's L2, so a GPU-scope fence
+// orders data before flag for them (fence_scope 0 = strict system scope).
 __device__ __forceinline__ void publish_tile(const LaunchParams& p, int64_t tile) {
-    if (!p.need_fence) return;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        fence_sys();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+        const long long c0 = p.prof ? clock64() : 0;
+        if (p.fence_scope == 0)
+            fence_sys();
+        else if (p.fence_scope == 1)
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * 8 + 6] += clock64() - c0;
+        const int w = threadIdx.x >> 5;
         for (int j = 0; j < p.n_jobs; ++j) {
             const DevJob& jb = p.jobs[j];
-            if (jb.produces) st_relaxed_sys(flag_ptr(p, jb.rank, slot_of(p, jb.version), tile), jb.version);
+            if (jb.produces) st_relaxed_sys(flag_ptr(p, jb.rank, tile, w), jb.version);
         }
     }
 }
@@ -669,7 +699,8 @@ __device__ __forceinline__ void tree_sum(const SmemCtl& sm, int pl, int log_leav
 }
 
 template <typename T>
-__device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, const typename Tr<T>::V* stage) {
+__device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, const typename Tr<T>::V* stage,
+                             long long* poll_cycles = nullptr) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
     constexpr int U = kVecPerThread;
@@ -678,18 +709,25 @@ __device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, c
     for (int pl = 0; pl < p.n_plans; ++pl) {
         const DevPlan& P_ = p.plans[pl];
         if (sm.plan_polls[pl]) {
-            // wait for the tiles peers are still producing (per-tile flags)
-            if (tid < P_.n_leaves && sm.leaf_src[pl][tid] == kSrcPoll) {
-                const int q = P_.leaves[tid];
+            const long long c0 = poll_cycles ? clock64() : 0;
+            // wait until the peer warps that mirror this warp published
+            // their part of the tile (per-warp flags, no CTA barrier)
+            const int lane = tid & 31, w = tid >> 5;
+            int rc = 0;
+            for (int li = lane; li < P_.n_leaves; li += 32) {
+                if (sm.leaf_src[pl][li] != kSrcPoll) continue;
+                const int q = P_.leaves[li];
                 const int64_t s = sm.stamps[P_.vidx][q];
-                const int rc = spin_eq(p, flag_ptr(p, q, sm.leaf_slot[pl][tid], tile), s, globaltimer());
+                rc = spin_geq(p, flag_ptr(p, q, tile, w), s, globaltimer());
                 if (rc) {
                     raise_error(p, rc, int64_t(q) << 32 | (tile & 0xffffffff));
                     sm.abort = 1;
+                    break;
                 }
             }
-            __syncthreads();
-            if (sm.abort) return false;
+            __syncwarp();
+            if (poll_cycles) *poll_cycles += clock64() - c0;
+            if (__any_sync(0xffffffffu, rc != 0) || sm.abort) return false;
         }
         V acc[U];
         tree_sum<T>(sm, pl, P_.log_leaves, tbase, stage, acc);
@@ -726,7 +764,7 @@ __device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, c
 // the fused step kernel (persistent: grid <= co-resident CTAs)
 // ---------------------------------------------------------------------------
 
-template <typename T>
+template <typename T, bool AHEAD>
 __global__ void __launch_bounds__(kThreads, 3) wagma_step_kernel(const __grid_constant__ LaunchParams p) {
     using V = typename Tr<T>::V;
     extern __shared__ __align__(16) unsigned char dyn_smem[];
@@ -741,15 +779,65 @@ __global__ void __launch_bounds__(kThreads, 3) wagma_step_kernel(const __grid_co
     }
     bool resolved = false;
     unsigned my_tiles = 0;
-    for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-        produce_tile<T>(p, tile, stage);
-        publish_tile(p, tile);
-        ++my_tiles;
-        if (!resolved) {
-            if (!resolve_sources<T>(p, sm)) break;
-            resolved = true;
+    if (!AHEAD) {
+        // one GPU: nobody outside this CTA waits for its tiles
+        for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+            produce_tile<T>(p, tile, stage);
+            ++my_tiles;
+            if (!resolved) {
+                if (!resolve_sources<T>(p, sm)) break;
+                resolved = true;
+            }
+            if (!consume_tile<T>(p, sm, tile, stage)) break;
         }
-        if (!consume_tile<T>(p, sm, tile, stage)) break;
+    } else {
+        // peers pull our tiles: produce one tile ahead (double-buffered
+        // stage) so a tile's flag is published a whole iteration before
+        // the peer CTA that mirrors this one needs it
+        V* stages[2] = {stage, stage + size_t(p.n_jobs) * kVecPerThread * kThreads};
+        const bool prof = p.prof != nullptr && threadIdx.x == 0;
+        long long cyc[6] = {0, 0, 0, 0, 0, 0};
+        long long c0 = prof ? clock64() : 0;
+        auto lap = [&](int i) {
+            if (prof) {
+                const long long c = clock64();
+                cyc[i] += c - c0;
+                c0 = c;
+            }
+        };
+        int64_t tile = blockIdx.x;
+        int buf = 0;
+        if (tile < p.n_tiles) {
+            produce_tile<T>(p, tile, stages[0]);
+            lap(0);
+            publish_tile(p, tile);
+            lap(1);
+            ++my_tiles;
+        }
+        while (tile < p.n_tiles) {
+            const int64_t next = tile + gridDim.x;
+            if (next < p.n_tiles) {
+                produce_tile<T>(p, next, stages[buf ^ 1]);
+                lap(0);
+                publish_tile(p, next);
+                lap(1);
+                ++my_tiles;
+            }
+            if (!resolved) {
+                if (!resolve_sources<T>(p, sm)) break;
+                resolved = true;
+                lap(2);
+            }
+            if (!consume_tile<T>(p, sm, tile, stages[buf], prof ? &cyc[3] : nullptr)) break;
+            lap(4);
+            tile = next;
+            buf ^= 1;
+        }
+        if (prof) {
+            cyc[4] -= cyc[3];
+            for (int i = 0; i < 5; ++i) p.prof[blockIdx.x * 8 + i] = cyc[i];
+            p.prof[blockIdx.x * 8 + 5] = my_tiles;
+        }
     }
     publish_slots(p, sm.abort ? 0u : my_tiles);
     if (blockIdx.x == 0) {
@@ -815,7 +903,9 @@ struct wg_ctx {
     wg_job_status* status_dev;
     int last_n_jobs;
     int sms;
-    int occ[kMaxJobs + 1];
+    int occ[2 * kMaxJobs + 1];
+    long long* prof;
+    int fence_scope;
 };
 
 extern "C" {
@@ -877,7 +967,7 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     L.desc = off;
     off = align_up(off + int64_t(ctx->Dv) * int64_t(sizeof(Desc)), 256);
     L.flags = off;
-    off = align_up(off + int64_t(ctx->R) * ctx->D * ctx->n_tiles * 8, 4096);
+    off = align_up(off + int64_t(ctx->R) * ctx->n_tiles * kWarps * 8, 4096);
     L.ring = off;
     off = align_up(off + int64_t(ctx->R) * ctx->D * ctx->npad * int64_t(ctx->esize), 4096);
     L.total = off;
@@ -896,7 +986,7 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
         };
         fill(L.announce, int64_t(ctx->R) * kAnnounceStride, -1);
         fill(L.complete, int64_t(ctx->R) * ctx->D, kNever);
-        fill(L.flags, int64_t(ctx->R) * ctx->D * ctx->n_tiles, kNever);
+        fill(L.flags, int64_t(ctx->R) * ctx->n_tiles * kWarps, kNever);
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "arena init: %s", cudaGetErrorString(e)); break; }
         e = cudaHostAlloc(&ctx->status_host, sizeof(wg_job_status) * kMaxJobs, cudaHostAllocMapped);
@@ -904,10 +994,14 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
         std::memset(ctx->status_host, 0, sizeof(wg_job_status) * kMaxJobs);
         e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->status_dev), ctx->status_host, 0);
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e)); break; }
-        const int max_smem = kMaxJobs * kThreads * kVecPerThread * 16;
-        e = cudaFuncSetAttribute(wagma_step_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+        const int max_smem = 2 * kMaxJobs * kThreads * kVecPerThread * 16;
+        e = cudaFuncSetAttribute(wagma_step_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(wagma_step_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+            e = cudaFuncSetAttribute(wagma_step_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(wagma_step_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(wagma_step_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)); break; }
         e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, c.device);
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "device attribute: %s", cudaGetErrorString(e)); break; }
@@ -920,6 +1014,11 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     }
     ctx->base[c.gpu_index] = ctx->arena;
     ctx->opened[c.gpu_index] = false;
+    ctx->fence_scope = 1;  // GPU scope for per-tile flags (see publish_tile)
+    if (const char* fs = getenv("WG_FENCE_SCOPE")) {
+        if (!strcmp(fs, "sys")) ctx->fence_scope = 0;
+        if (!strcmp(fs, "none")) ctx->fence_scope = 2;  // timing experiments only: unsafe
+    }
     *out = ctx;
     return WG_OK;
 }
@@ -992,8 +1091,8 @@ int wg_ctx_set_initial_model(wg_ctx* ctx, int rank, const void* w0, void* stream
     char* slot0 = ctx->arena + ctx->L.ring + (int64_t(l) * ctx->D + 0) * ctx->npad * int64_t(ctx->esize);
     WG_CUDA(cudaMemsetAsync(slot0, 0, size_t(ctx->npad) * ctx->esize, s));
     if (ctx->cfg.n > 0) WG_CUDA(cudaMemcpyAsync(slot0, w0, size_t(ctx->cfg.n) * ctx->esize, cudaMemcpyDeviceToDevice, s));
-    int64_t* flags0 = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.flags) + (int64_t(l) * ctx->D + 0) * ctx->n_tiles;
-    fill_i64_kernel<<<64, 256, 0, s>>>(flags0, ctx->n_tiles, -1);
+    int64_t* flags0 = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.flags) + int64_t(l) * ctx->n_tiles * kWarps;
+    fill_i64_kernel<<<64, 256, 0, s>>>(flags0, ctx->n_tiles * kWarps, -1);
     int64_t* comp = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.complete) + int64_t(l) * ctx->D + 0;
     fill_i64_kernel<<<1, 32, 0, s>>>(comp, 1, -1);
     WG_CUDA(cudaGetLastError());
@@ -1010,8 +1109,8 @@ int wg_install(wg_ctx* ctx, int rank, int64_t stamp, const void* vec, void* stre
     const int slot = int((stamp + 1) % ctx->D);
     char* dst = ctx->arena + ctx->L.ring + (int64_t(l) * ctx->D + slot) * ctx->npad * int64_t(ctx->esize);
     if (ctx->cfg.n > 0) WG_CUDA(cudaMemcpyAsync(dst, vec, size_t(ctx->cfg.n) * ctx->esize, cudaMemcpyDeviceToDevice, s));
-    int64_t* flags = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.flags) + (int64_t(l) * ctx->D + slot) * ctx->n_tiles;
-    fill_i64_kernel<<<64, 256, 0, s>>>(flags, ctx->n_tiles, stamp);
+    int64_t* flags = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.flags) + int64_t(l) * ctx->n_tiles * kWarps;
+    fill_i64_kernel<<<64, 256, 0, s>>>(flags, ctx->n_tiles * kWarps, stamp);
     int64_t* comp = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.complete) + int64_t(l) * ctx->D + slot;
     fill_i64_kernel<<<1, 32, 0, s>>>(comp, 1, stamp);
     int64_t* ann = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.announce) + int64_t(l) * kAnnounceStride;
@@ -1040,9 +1139,14 @@ static int occupancy(wg_ctx* ctx, int n_stage) {
     if (ctx->occ[n_stage] > 0) return ctx->occ[n_stage];
     int occ = 0;
     const size_t smem = size_t(n_stage) * kThreads * kVecPerThread * 16;
-    cudaError_t e = ctx->cfg.dtype == WG_F32
-                        ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wagma_step_kernel<float>, kThreads, smem)
-                        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wagma_step_kernel<double>, kThreads, smem);
+    const bool ahead = ctx->cfg.n_gpus > 1;
+    cudaError_t e;
+    if (ctx->cfg.dtype == WG_F32)
+        e = ahead ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wagma_step_kernel<float, true>, kThreads, smem)
+                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wagma_step_kernel<float, false>, kThreads, smem);
+    else
+        e = ahead ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wagma_step_kernel<double, true>, kThreads, smem)
+                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wagma_step_kernel<double, false>, kThreads, smem);
     if (e != cudaSuccess || occ < 1) occ = 1;
     ctx->occ[n_stage] = occ;
     return occ;
@@ -1078,6 +1182,8 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
     p.timeout_ns = c.timeout_ns;
     p.staleness_bound = c.staleness_bound;
     p.status = ctx->status_dev;
+    p.prof = ctx->prof;
+    p.fence_scope = ctx->fence_scope;
     for (int q = 0; q < kMaxP; ++q) p.job_of_rank[q] = -1;
 
     const size_t align_mask = 15;
@@ -1213,17 +1319,25 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         }
     }
 
-    int n_stage = 0;
-    for (int j = 0; j < n_jobs; ++j) n_stage = std::max(n_stage, p.jobs[j].produces ? j + 1 : 0);
-    const size_t smem = size_t(std::max(n_stage, 1)) * kThreads * kVecPerThread * 16;
-    const int occ = occupancy(ctx, std::max(n_stage, 1));
+    // shared-memory stage: one 16-byte vector per thread per job (x2 when
+    // tiles are produced one ahead for peers on other GPUs)
+    const int n_stage = n_jobs * (p.need_fence ? 2 : 1);
+    const size_t smem = size_t(n_stage) * kThreads * kVecPerThread * 16;
+    const int occ = occupancy(ctx, n_stage);
     const int64_t grid = std::min<int64_t>(ctx->n_tiles, int64_t(occ) * ctx->sms);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     WG_CUDA(cudaSetDevice(c.device));
-    if (c.dtype == WG_F32)
-        wagma_step_kernel<float><<<unsigned(grid), kThreads, smem, s>>>(p);
-    else
-        wagma_step_kernel<double><<<unsigned(grid), kThreads, smem, s>>>(p);
+    if (c.dtype == WG_F32) {
+        if (p.need_fence)
+            wagma_step_kernel<float, true><<<unsigned(grid), kThreads, smem, s>>>(p);
+        else
+            wagma_step_kernel<float, false><<<unsigned(grid), kThreads, smem, s>>>(p);
+    } else {
+        if (p.need_fence)
+            wagma_step_kernel<double, true><<<unsigned(grid), kThreads, smem, s>>>(p);
+        else
+            wagma_step_kernel<double, false><<<unsigned(grid), kThreads, smem, s>>>(p);
+    }
     WG_CUDA(cudaGetLastError());
     ctx->last_n_jobs = n_jobs;
     return WG_OK;
@@ -1274,11 +1388,17 @@ int wg_delay(wg_ctx* ctx, int64_t ns, void* stream) {
     return WG_OK;
 }
 
+int wg_ctx_set_profile(wg_ctx* ctx, void* dev_buf) {
+    if (!ctx) return fail(WG_EINVAL, "null ctx");
+    ctx->prof = static_cast<long long*>(dev_buf);
+    return WG_OK;
+}
+
 int wg_ctx_geometry(wg_ctx* ctx, int64_t* tile_elems, int64_t* n_tiles, int* grid, int* ring_depth) {
     if (!ctx) return fail(WG_EINVAL, "null ctx");
     if (tile_elems) *tile_elems = ctx->tile_elems;
     if (n_tiles) *n_tiles = ctx->n_tiles;
-    if (grid) *grid = int(std::min<int64_t>(ctx->n_tiles, int64_t(occupancy(ctx, ctx->R)) * ctx->sms));
+    if (grid) *grid = int(std::min<int64_t>(ctx->n_tiles, int64_t(occupancy(ctx, ctx->R * (ctx->cfg.n_gpus > 1 ? 2 : 1))) * ctx->sms));
     if (ring_depth) *ring_depth = ctx->D;
     return WG_OK;
 }

@@ -1,0 +1,56 @@
+"""Per-CTA phase breakdown of the multi-GPU step kernel (device clock64 counters).
+
+torchrun --nproc-per-node N tools/phase_profile.py [--S 8] [--P 8] [--n N]
+Prints, per rank, the mean over CTAs of cycles spent producing, publishing
+(barrier + system fence + flags), resolving sources, polling peer flags and
+consuming, for a group step and a sync step.
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2005_00124_b200.context import DeviceContext  # noqa: E402
+from paper_2005_00124_b200.optim import EtaSchedule, GroupAveragingOptimizer, OptimizerConfig  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--P", type=int, default=8)
+ap.add_argument("--S", type=int, default=8)
+ap.add_argument("--nelem", type=int, default=25_559_081)
+ap.add_argument("--tau", type=int, default=10)
+ap.add_argument("--iters", type=int, default=30)
+a = ap.parse_args()
+rank, G, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+torch.cuda.set_device(local)
+dev = torch.device("cuda", local)
+dist.init_process_group("nccl", device_id=dev)
+ctx = DeviceContext(a.P, a.S, a.nelem, tau=a.tau, n_gpus=G, gpu_index=rank, device=local)
+opt = GroupAveragingOptimizer(ctx, OptimizerConfig(T=1 << 30, S=a.S, tau=a.tau, eta=EtaSchedule(value=0.1),
+                                                   update_rule="momentum"), torch.zeros(a.nelem, device=dev))
+g = {r: torch.randn(a.nelem, device=dev) * 0.01 for r in ctx.local_ranks}
+prof = torch.zeros(ctx.grid * 8, dtype=torch.int64, device=dev)
+ctx.lib.wg_ctx_set_profile(ctx._h, ctypes.c_void_p(prof.data_ptr()))
+ghz = 1.965
+for t in range(a.iters):
+    prof.zero_()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    opt.step(t, g)
+    ev1.record()
+    torch.cuda.synchronize()
+    if t >= a.iters - a.tau:
+        p = prof.view(-1, 8).cpu().numpy().astype(np.float64)
+        names = ["produce", "publish", "resolve", "poll", "consume", "tiles", "fence"]
+        us = {nm: p[:, i].mean() / ghz / 1000 for i, nm in enumerate(names) if nm != "tiles"}
+        sync = (t + 1) % a.tau == 0
+        print(f"rank{rank} t={t} {'sync ' if sync else 'group'} kernel={ev0.elapsed_time(ev1)*1000:.0f}us tiles/CTA={p[:,5].mean():.1f} "
+              + " ".join(f"{k}={v:.0f}" for k, v in us.items()), flush=True)
+ctx.lib.wg_ctx_set_profile(ctx._h, None)
+ctx.check()
+dist.barrier()
+dist.destroy_process_group()
