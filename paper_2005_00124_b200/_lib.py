@@ -88,7 +88,8 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.LIB_PATH
+    # WAGMA_B200_LIB: load an alternative build (A/B kernel experiments)
+    return os.environ.get("WAGMA_B200_LIB", _build.LIB_PATH)
 
 
 def load(build_if_missing: bool = False) -> ctypes.CDLL:
@@ -105,7 +106,11 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
         _build.build()
     lib = ctypes.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None and "WAGMA_B200_LIB" in os.environ:
+            continue  # older experimental build without this entry point
+        if fn is None:
+            raise ImportError(f"{path} does not export {name}")
         fn.restype = res
         fn.argtypes = args
     _lib = lib

@@ -79,7 +79,7 @@ class _SlotView:
 
     def __init__(self, ptr: int, n: int, dtype: torch.dtype):
         typestr = "<f4" if dtype == torch.float32 else "<f8"
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, True),
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
                                          "version": 3, "strides": None}
 
 

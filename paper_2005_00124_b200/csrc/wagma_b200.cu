@@ -33,6 +33,13 @@
 #include "../../include/wagma_b200.h"
 #include "wagma_internal.h"
 
+#ifndef WG_MINB
+#define WG_MINB 3  // CTAs per SM the single-GPU kernel is register-budgeted for
+#endif
+#ifndef WG_MINB_AHEAD
+#define WG_MINB_AHEAD 3
+#endif
+
 namespace wg {
 
 // ---------------------------------------------------------------------------
@@ -398,7 +405,6 @@ enum LeafSrc : int8_t { kSrcPoll = -1, kSrcReady = -2 };
 
 struct SmemCtl {
     int64_t stamps[kMaxVersions][kMaxP];     // contribution stamps per version
-    const void* leaf_ptr[kMaxPlans][kMaxLeaves];
     int8_t leaf_src[kMaxPlans][kMaxLeaves];  // >=0: stage of job; -1 poll; -2 ready
     int16_t leaf_slot[kMaxPlans][kMaxLeaves];
     int32_t plan_polls[kMaxPlans];
@@ -463,7 +469,6 @@ __device__ bool resolve_sources(const LaunchParams& p, SmemCtl& sm) {
                 sm.abort = 1;
             }
             src = (c == s) ? int8_t(kSrcReady) : int8_t(kSrcPoll);
-            sm.leaf_ptr[pl][li] = ring_ptr<T>(p, q, slot);
             sm.leaf_slot[pl][li] = int16_t(slot);
         }
         sm.leaf_src[pl][li] = src;
@@ -482,6 +487,83 @@ __device__ bool resolve_sources(const LaunchParams& p, SmemCtl& sm) {
 // produce: local step, send-ring install, shared-memory stage
 // ---------------------------------------------------------------------------
 
+// Inputs are streamed through a per-thread shared-memory ring with cp.async
+// (LDGSTS): each thread prefetches the W, g, m vectors of the next kDepth
+// (tile, job) items it will compute, so memory-level parallelism does not
+// depend on registers. A thread only ever reads the ring entries it filled
+// itself, so no barrier is needed (cp.async.wait_group orders its own copies).
+#ifndef WG_DEPTH
+#define WG_DEPTH 3
+#endif
+constexpr int kDepth = WG_DEPTH;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gsrc), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Prefetch one item's inputs (zero-filled past n: the ragged end).
+template <typename T>
+__device__ __forceinline__ void issue_item(const LaunchParams& p, int64_t tile, int j, typename Tr<T>::V* slot) {
+    constexpr int E = Tr<T>::EPV;
+    const int tid = threadIdx.x;
+    const int64_t idx = tile * p.tile_elems + int64_t(tid) * E;
+    const int64_t rem = p.n - idx;
+    const int bytes = rem >= E ? 16 : (rem > 0 ? int(rem * int64_t(sizeof(T))) : 0);
+    const int64_t off = bytes ? idx : 0;
+    const DevJob& jb = p.jobs[j];
+    if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
+        cp_async16(&slot[tid], static_cast<const T*>(jb.fresh) + off, bytes);
+        return;
+    }
+    cp_async16(&slot[tid], static_cast<const T*>(jb.W) + off, bytes);
+    cp_async16(&slot[kThreads + tid], static_cast<const T*>(jb.g) + off, bytes);
+    if (jb.update_rule == WG_UPDATE_MOMENTUM)
+        cp_async16(&slot[2 * kThreads + tid], static_cast<const T*>(jb.m) + off, bytes);
+}
+
+// Local step of one item + send-ring install + stage (optim.py:176-183,
+// collective.py:95-101).
+template <typename T>
+__device__ __forceinline__ void compute_item(const LaunchParams& p, int64_t tile, int j,
+                                             const typename Tr<T>::V* slot, typename Tr<T>::V* stage) {
+    using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
+    const int tid = threadIdx.x;
+    const int64_t idx = tile * p.tile_elems + int64_t(tid) * E;
+    const DevJob& jb = p.jobs[j];
+    V wp;
+    if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
+        wp = slot[tid];
+    } else {
+        const V w = slot[tid];
+        const V g = slot[kThreads + tid];
+        const T eta = T(jb.eta);
+        if (jb.update_rule == WG_UPDATE_MOMENTUM) {
+            // m = beta*m + g ; W' = W - eta*m  (optim.py:179,183)
+            const V mn = vadd(vscale(T(jb.beta), slot[2 * kThreads + tid]), g);
+            st_stream<T>(static_cast<T*>(jb.m), idx, p.n, mn);
+            wp = vsub(w, vscale(eta, mn));
+        } else {
+            wp = vsub(w, vscale(eta, g));  // W' = W - eta*g (optim.py:181-183)
+        }
+        if (jb.kind == WG_JOB_LOCAL_STEP) {
+            st_stream<T>(static_cast<T*>(jb.W), idx, p.n, wp);
+            return;
+        }
+    }
+    // SendBuffer.install: W' written once into the send ring, and staged
+    __stcg(reinterpret_cast<V*>(ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + idx), wp);
+    stage[j * kThreads + tid] = wp;
+}
+
+// Multi-GPU kernel: register-pipelined produce (the next job's loads in
+// flight while the current one computes); keeps 3 CTAs/SM for NVLink latency.
 // Loads of one job's inputs for this thread's vectors of a tile.
 template <typename T>
 __device__ __forceinline__ void load_job(const LaunchParams& p, const DevJob& jb, int64_t tbase,
@@ -510,7 +592,7 @@ __device__ __forceinline__ void load_job(const LaunchParams& p, const DevJob& jb
 }
 
 template <typename T>
-__device__ __forceinline__ void produce_tile(const LaunchParams& p, int64_t tile, typename Tr<T>::V* stage) {
+__device__ __forceinline__ void produce_tile_regs(const LaunchParams& p, int64_t tile, typename Tr<T>::V* stage) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
     constexpr int U = kVecPerThread;
@@ -617,11 +699,11 @@ __device__ __forceinline__ void publish_slots(const LaunchParams& p, unsigned my
 template <typename T, int LOG>
 struct TreeSum {
     using V = typename Tr<T>::V;
-    static __device__ __forceinline__ void run(const SmemCtl& sm, int pl, int leaf0, int64_t toff,
-                                               const V* stage, V* out) {
+    static __device__ __forceinline__ void run(const LaunchParams& p, const SmemCtl& sm, int pl, int leaf0,
+                                               int64_t toff, const V* stage, V* out) {
         V a[kVecPerThread], b[kVecPerThread];
-        TreeSum<T, LOG - 1>::run(sm, pl, leaf0, toff, stage, a);
-        TreeSum<T, LOG - 1>::run(sm, pl, leaf0 + (1 << (LOG - 1)), toff, stage, b);
+        TreeSum<T, LOG - 1>::run(p, sm, pl, leaf0, toff, stage, a);
+        TreeSum<T, LOG - 1>::run(p, sm, pl, leaf0 + (1 << (LOG - 1)), toff, stage, b);
 #pragma unroll
         for (int k = 0; k < kVecPerThread; ++k) out[k] = vadd(a[k], b[k]);
     }
@@ -629,8 +711,8 @@ struct TreeSum {
 template <typename T>
 struct TreeSum<T, 0> {
     using V = typename Tr<T>::V;
-    static __device__ __forceinline__ void run(const SmemCtl& sm, int pl, int leaf, int64_t toff,
-                                               const V* stage, V* out) {
+    static __device__ __forceinline__ void run(const LaunchParams& p, const SmemCtl& sm, int pl, int leaf,
+                                               int64_t toff, const V* stage, V* out) {
         constexpr int E = Tr<T>::EPV;
         const int src = sm.leaf_src[pl][leaf];
         const int tid = threadIdx.x;
@@ -640,7 +722,7 @@ struct TreeSum<T, 0> {
         } else {
             // 128-bit loads of a peer's (NVLink) or an older local send slot;
             // .cg: L2 only, never a stale L1 line of a re-published slot.
-            const T* base = static_cast<const T*>(sm.leaf_ptr[pl][leaf]) + toff;
+            const T* base = ring_ptr<T>(p, p.plans[pl].leaves[leaf], sm.leaf_slot[pl][leaf]) + toff;
 #pragma unroll
             for (int k = 0; k < kVecPerThread; ++k)
                 out[k] = __ldcg(reinterpret_cast<const V*>(base + int64_t(k * kThreads + tid) * E));
@@ -651,7 +733,7 @@ struct TreeSum<T, 0> {
 // Trees of 16..64 leaves: 8-leaf subtrees combined through a 4-level
 // register stack (static indices only), same pairing as the full tree.
 template <typename T>
-__device__ __noinline__ void tree_sum_big(const SmemCtl& sm, int pl, int log_leaves, int64_t toff,
+__device__ __noinline__ void tree_sum_big(const LaunchParams& p, const SmemCtl& sm, int pl, int log_leaves, int64_t toff,
                                           const typename Tr<T>::V* stage, typename Tr<T>::V* out) {
     using V = typename Tr<T>::V;
     constexpr int U = kVecPerThread;
@@ -659,7 +741,7 @@ __device__ __noinline__ void tree_sum_big(const SmemCtl& sm, int pl, int log_lea
     const int nchunks = 1 << (log_leaves - 3);
     for (int c = 0; c < nchunks; ++c) {
         V cur[U];
-        TreeSum<T, 3>::run(sm, pl, c * 8, toff, stage, cur);
+        TreeSum<T, 3>::run(p, sm, pl, c * 8, toff, stage, cur);
         if (!(c & 1)) {
 #pragma unroll
             for (int k = 0; k < U; ++k) s0[k] = cur[k];
@@ -687,14 +769,14 @@ __device__ __noinline__ void tree_sum_big(const SmemCtl& sm, int pl, int log_lea
 }
 
 template <typename T>
-__device__ __forceinline__ void tree_sum(const SmemCtl& sm, int pl, int log_leaves, int64_t toff,
-                                         const typename Tr<T>::V* stage, typename Tr<T>::V* out) {
+__device__ __forceinline__ void tree_sum(const LaunchParams& p, const SmemCtl& sm, int pl, int log_leaves,
+                                         int64_t toff, const typename Tr<T>::V* stage, typename Tr<T>::V* out) {
     switch (log_leaves) {
-        case 0: TreeSum<T, 0>::run(sm, pl, 0, toff, stage, out); break;
-        case 1: TreeSum<T, 1>::run(sm, pl, 0, toff, stage, out); break;
-        case 2: TreeSum<T, 2>::run(sm, pl, 0, toff, stage, out); break;
-        case 3: TreeSum<T, 3>::run(sm, pl, 0, toff, stage, out); break;
-        default: tree_sum_big<T>(sm, pl, log_leaves, toff, stage, out); break;
+        case 0: TreeSum<T, 0>::run(p, sm, pl, 0, toff, stage, out); break;
+        case 1: TreeSum<T, 1>::run(p, sm, pl, 0, toff, stage, out); break;
+        case 2: TreeSum<T, 2>::run(p, sm, pl, 0, toff, stage, out); break;
+        case 3: TreeSum<T, 3>::run(p, sm, pl, 0, toff, stage, out); break;
+        default: tree_sum_big<T>(p, sm, pl, log_leaves, toff, stage, out); break;
     }
 }
 
@@ -730,7 +812,7 @@ __device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, c
             if (__any_sync(0xffffffffu, rc != 0) || sm.abort) return false;
         }
         V acc[U];
-        tree_sum<T>(sm, pl, P_.log_leaves, tbase, stage, acc);
+        tree_sum<T>(p, sm, pl, P_.log_leaves, tbase, stage, acc);
         // timely members share one result: acc/S or total/P (optim.py:442,452);
         // a power-of-two divisor is an exact reciprocal multiply (same IEEE result)
         V avg[U];
@@ -765,7 +847,7 @@ __device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, c
 // ---------------------------------------------------------------------------
 
 template <typename T, bool AHEAD>
-__global__ void __launch_bounds__(kThreads, 3) wagma_step_kernel(const __grid_constant__ LaunchParams p) {
+__global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wagma_step_kernel(const __grid_constant__ LaunchParams p) {
     using V = typename Tr<T>::V;
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     V* stage = reinterpret_cast<V*>(dyn_smem);
@@ -779,21 +861,7 @@ __global__ void __launch_bounds__(kThreads, 3) wagma_step_kernel(const __grid_co
     }
     bool resolved = false;
     unsigned my_tiles = 0;
-    if (!AHEAD) {
-        // one GPU: nobody outside this CTA waits for its tiles
-        for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-            produce_tile<T>(p, tile, stage);
-            ++my_tiles;
-            if (!resolved) {
-                if (!resolve_sources<T>(p, sm)) break;
-                resolved = true;
-            }
-            if (!consume_tile<T>(p, sm, tile, stage)) break;
-        }
-    } else {
-        // peers pull our tiles: produce one tile ahead (double-buffered
-        // stage) so a tile's flag is published a whole iteration before
-        // the peer CTA that mirrors this one needs it
+    if constexpr (AHEAD) {
         V* stages[2] = {stage, stage + size_t(p.n_jobs) * kVecPerThread * kThreads};
         const bool prof = p.prof != nullptr && threadIdx.x == 0;
         long long cyc[6] = {0, 0, 0, 0, 0, 0};
@@ -808,7 +876,7 @@ __global__ void __launch_bounds__(kThreads, 3) wagma_step_kernel(const __grid_co
         int64_t tile = blockIdx.x;
         int buf = 0;
         if (tile < p.n_tiles) {
-            produce_tile<T>(p, tile, stages[0]);
+            produce_tile_regs<T>(p, tile, stages[0]);
             lap(0);
             publish_tile(p, tile);
             lap(1);
@@ -817,7 +885,7 @@ __global__ void __launch_bounds__(kThreads, 3) wagma_step_kernel(const __grid_co
         while (tile < p.n_tiles) {
             const int64_t next = tile + gridDim.x;
             if (next < p.n_tiles) {
-                produce_tile<T>(p, next, stages[buf ^ 1]);
+                produce_tile_regs<T>(p, next, stages[buf ^ 1]);
                 lap(0);
                 publish_tile(p, next);
                 lap(1);
@@ -838,6 +906,76 @@ __global__ void __launch_bounds__(kThreads, 3) wagma_step_kernel(const __grid_co
             for (int i = 0; i < 5; ++i) p.prof[blockIdx.x * 8 + i] = cyc[i];
             p.prof[blockIdx.x * 8 + 5] = my_tiles;
         }
+    } else {
+    const int J = p.n_jobs;
+    V* ring = stage;  // [kDepth][3][kThreads]
+    V* stages[2] = {ring + kDepth * 3 * kThreads, ring + kDepth * 3 * kThreads + size_t(J) * kThreads};
+    const int64_t my_ntiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t n_items = my_ntiles * J;
+    const bool prof = AHEAD && p.prof != nullptr && threadIdx.x == 0;
+    long long cyc[6] = {0, 0, 0, 0, 0, 0};
+    long long c0 = prof ? clock64() : 0;
+    auto lap = [&](int i) {
+        if (prof) {
+            const long long c = clock64();
+            cyc[i] += c - c0;
+            c0 = c;
+        }
+    };
+    auto item_tile = [&](int64_t i) { return int64_t(blockIdx.x) + (i / J) * int64_t(gridDim.x); };
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d) {
+        if (d < n_items) issue_item<T>(p, item_tile(d), int(d % J), ring + d * 3 * kThreads);
+        cp_async_commit();
+    }
+    int64_t i = 0;
+    bool ok = true;
+    for (int64_t kk = 0; kk < my_ntiles && ok; ++kk) {
+        const int64_t tile = int64_t(blockIdx.x) + kk * gridDim.x;
+        V* st = stages[AHEAD ? (kk & 1) : 0];
+        for (int j = 0; j < J; ++j, ++i) {
+            cp_async_wait<kDepth - 1>();
+            V* slot = ring + (i % kDepth) * 3 * kThreads;
+            compute_item<T>(p, tile, j, slot, st);
+            if (i + kDepth < n_items) issue_item<T>(p, item_tile(i + kDepth), int((i + kDepth) % J), slot);
+            cp_async_commit();
+        }
+        ++my_tiles;
+        lap(0);
+        if (AHEAD) {
+            // peers pull our tiles: publish now, consume the previous tile so
+            // a flag is out a whole tile before the mirroring peer CTA needs it
+            publish_tile(p, tile);
+            lap(1);
+            if (kk == 0) continue;
+        }
+        if (!resolved) {
+            if (!resolve_sources<T>(p, sm)) {
+                ok = false;
+                break;
+            }
+            resolved = true;
+            lap(2);
+        }
+        const int64_t ctile = AHEAD ? tile - gridDim.x : tile;
+        V* cst = AHEAD ? stages[(kk - 1) & 1] : st;
+        if (!consume_tile<T>(p, sm, ctile, cst, prof ? &cyc[3] : nullptr)) ok = false;
+        lap(4);
+    }
+    if (AHEAD && ok && my_ntiles > 0) {
+        if (!resolved) resolved = resolve_sources<T>(p, sm);
+        if (resolved) {
+            const int64_t last = int64_t(blockIdx.x) + (my_ntiles - 1) * gridDim.x;
+            consume_tile<T>(p, sm, last, stages[(my_ntiles - 1) & 1], prof ? &cyc[3] : nullptr);
+            lap(4);
+        }
+    }
+    cp_async_wait<0>();
+    if (prof) {
+        cyc[4] -= cyc[3];
+        for (int q = 0; q < 5; ++q) p.prof[blockIdx.x * 8 + q] = cyc[q];
+        p.prof[blockIdx.x * 8 + 5] = my_tiles;
+    }
     }
     publish_slots(p, sm.abort ? 0u : my_tiles);
     if (blockIdx.x == 0) {
@@ -871,6 +1009,9 @@ __global__ void delay_kernel(int64_t ns) {
 // ---------------------------------------------------------------------------
 
 static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+static size_t dyn_smem_bytes(int n_stage, bool ahead) {
+    return size_t((ahead ? 0 : kDepth * 3) + n_stage) * kThreads * 16;
+}
 static bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
 static int ilog2(int64_t n) {
     int r = 0;
@@ -994,7 +1135,7 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
         std::memset(ctx->status_host, 0, sizeof(wg_job_status) * kMaxJobs);
         e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->status_dev), ctx->status_host, 0);
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e)); break; }
-        const int max_smem = 2 * kMaxJobs * kThreads * kVecPerThread * 16;
+        const int max_smem = int(dyn_smem_bytes(2 * kMaxJobs, false));
         e = cudaFuncSetAttribute(wagma_step_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(wagma_step_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
@@ -1138,7 +1279,7 @@ int wg_ctx_slot(wg_ctx* ctx, int rank, int64_t stamp, void** ptr, int64_t* held_
 static int occupancy(wg_ctx* ctx, int n_stage) {
     if (ctx->occ[n_stage] > 0) return ctx->occ[n_stage];
     int occ = 0;
-    const size_t smem = size_t(n_stage) * kThreads * kVecPerThread * 16;
+    const size_t smem = dyn_smem_bytes(n_stage, ctx->cfg.n_gpus > 1);
     const bool ahead = ctx->cfg.n_gpus > 1;
     cudaError_t e;
     if (ctx->cfg.dtype == WG_F32)
@@ -1319,10 +1460,11 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         }
     }
 
-    // shared-memory stage: one 16-byte vector per thread per job (x2 when
-    // tiles are produced one ahead for peers on other GPUs)
+    // dynamic shared memory: the cp.async input ring + one 16-byte stage
+    // vector per thread per job (x2 when tiles are produced one ahead for
+    // peers on other GPUs)
     const int n_stage = n_jobs * (p.need_fence ? 2 : 1);
-    const size_t smem = size_t(n_stage) * kThreads * kVecPerThread * 16;
+    const size_t smem = dyn_smem_bytes(n_stage, p.need_fence);
     const int occ = occupancy(ctx, n_stage);
     const int64_t grid = std::min<int64_t>(ctx->n_tiles, int64_t(occ) * ctx->sms);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
