@@ -211,30 +211,40 @@ __device__ __forceinline__ double2 vdiv(double2 a, double d) {
 }
 
 // Caller-owned vectors (W, m, g, fresh, acc_out) have exactly n elements:
-// full 16-byte vectors inside, element-wise handling of the ragged end.
+// full 16-byte vectors inside, element-wise handling of the ragged end
+// (component by component: no address of a register vector is taken).
+__device__ __forceinline__ float4 ld_tail(const float* b, int64_t idx, int64_t n) {
+    return make_float4(idx < n ? b[idx] : 0.f, idx + 1 < n ? b[idx + 1] : 0.f, idx + 2 < n ? b[idx + 2] : 0.f,
+                       idx + 3 < n ? b[idx + 3] : 0.f);
+}
+__device__ __forceinline__ double2 ld_tail(const double* b, int64_t idx, int64_t n) {
+    return make_double2(idx < n ? b[idx] : 0.0, idx + 1 < n ? b[idx + 1] : 0.0);
+}
+__device__ __forceinline__ void st_tail(float* b, int64_t idx, int64_t n, float4 v) {
+    if (idx < n) b[idx] = v.x;
+    if (idx + 1 < n) b[idx + 1] = v.y;
+    if (idx + 2 < n) b[idx + 2] = v.z;
+    if (idx + 3 < n) b[idx + 3] = v.w;
+}
+__device__ __forceinline__ void st_tail(double* b, int64_t idx, int64_t n, double2 v) {
+    if (idx < n) b[idx] = v.x;
+    if (idx + 1 < n) b[idx + 1] = v.y;
+}
 template <typename T, bool FULL = false>
 __device__ __forceinline__ typename Tr<T>::V ld_stream(const T* base, int64_t idx, int64_t n) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
     if (FULL || idx + E <= n) return __ldcs(reinterpret_cast<const V*>(base + idx));
-    V v;
-    T* e = reinterpret_cast<T*>(&v);
-#pragma unroll
-    for (int i = 0; i < E; ++i) e[i] = (idx + i < n) ? base[idx + i] : T(0);
-    return v;
+    return ld_tail(base, idx, n);
 }
 template <typename T, bool FULL = false>
 __device__ __forceinline__ void st_stream(T* base, int64_t idx, int64_t n, typename Tr<T>::V v) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
-    if (FULL || idx + E <= n) {
+    if (FULL || idx + E <= n)
         __stcs(reinterpret_cast<V*>(base + idx), v);
-        return;
-    }
-    const T* e = reinterpret_cast<const T*>(&v);
-#pragma unroll
-    for (int i = 0; i < E; ++i)
-        if (idx + i < n) base[idx + i] = e[i];
+    else
+        st_tail(base, idx, n, v);
 }
 
 // ---------------------------------------------------------------------------
@@ -696,87 +706,72 @@ __device__ __forceinline__ void publish_slots(const LaunchParams& p, unsigned my
 // consume: butterfly-tree sum of the group's leaves, averaging rule
 // ---------------------------------------------------------------------------
 
+static_assert(kVecPerThread == 1, "the consume path is written for one 16-byte vector per thread");
+
 template <typename T, int LOG>
 struct TreeSum {
     using V = typename Tr<T>::V;
-    static __device__ __forceinline__ void run(const LaunchParams& p, const SmemCtl& sm, int pl, int leaf0,
-                                               int64_t toff, const V* stage, V* out) {
-        V a[kVecPerThread], b[kVecPerThread];
-        TreeSum<T, LOG - 1>::run(p, sm, pl, leaf0, toff, stage, a);
-        TreeSum<T, LOG - 1>::run(p, sm, pl, leaf0 + (1 << (LOG - 1)), toff, stage, b);
-#pragma unroll
-        for (int k = 0; k < kVecPerThread; ++k) out[k] = vadd(a[k], b[k]);
+    static __device__ __forceinline__ V run(const LaunchParams& p, const SmemCtl& sm, int pl, int leaf0,
+                                            int64_t toff, const V* stage) {
+        const V a = TreeSum<T, LOG - 1>::run(p, sm, pl, leaf0, toff, stage);
+        const V b = TreeSum<T, LOG - 1>::run(p, sm, pl, leaf0 + (1 << (LOG - 1)), toff, stage);
+        return vadd(a, b);
     }
 };
 template <typename T>
 struct TreeSum<T, 0> {
     using V = typename Tr<T>::V;
-    static __device__ __forceinline__ void run(const LaunchParams& p, const SmemCtl& sm, int pl, int leaf,
-                                               int64_t toff, const V* stage, V* out) {
+    static __device__ __forceinline__ V run(const LaunchParams& p, const SmemCtl& sm, int pl, int leaf,
+                                            int64_t toff, const V* stage) {
         constexpr int E = Tr<T>::EPV;
         const int src = sm.leaf_src[pl][leaf];
         const int tid = threadIdx.x;
-        if (src >= 0) {
-#pragma unroll
-            for (int k = 0; k < kVecPerThread; ++k) out[k] = stage[(src * kVecPerThread + k) * kThreads + tid];
-        } else {
-            // 128-bit loads of a peer's (NVLink) or an older local send slot;
-            // .cg: L2 only, never a stale L1 line of a re-published slot.
-            const T* base = ring_ptr<T>(p, p.plans[pl].leaves[leaf], sm.leaf_slot[pl][leaf]) + toff;
-#pragma unroll
-            for (int k = 0; k < kVecPerThread; ++k)
-                out[k] = __ldcg(reinterpret_cast<const V*>(base + int64_t(k * kThreads + tid) * E));
-        }
+        if (src >= 0) return stage[src * kThreads + tid];
+        // 128-bit load of a peer's (NVLink) or an older local send slot;
+        // .cg: L2 only, never a stale L1 line of a re-published slot.
+        const T* base = ring_ptr<T>(p, p.plans[pl].leaves[leaf], sm.leaf_slot[pl][leaf]) + toff;
+        return __ldcg(reinterpret_cast<const V*>(base + int64_t(tid) * E));
     }
 };
 
 // Trees of 16..64 leaves: 8-leaf subtrees combined through a 4-level
 // register stack (static indices only), same pairing as the full tree.
 template <typename T>
-__device__ __noinline__ void tree_sum_big(const LaunchParams& p, const SmemCtl& sm, int pl, int log_leaves, int64_t toff,
-                                          const typename Tr<T>::V* stage, typename Tr<T>::V* out) {
+__device__ __noinline__ typename Tr<T>::V tree_sum_big(const LaunchParams& p, const SmemCtl& sm, int pl,
+                                                       int log_leaves, int64_t toff, const typename Tr<T>::V* stage) {
     using V = typename Tr<T>::V;
-    constexpr int U = kVecPerThread;
-    V s0[U], s1[U], s2[U], s3[U];
+    V s0, s1, s2, s3;
     const int nchunks = 1 << (log_leaves - 3);
     for (int c = 0; c < nchunks; ++c) {
-        V cur[U];
-        TreeSum<T, 3>::run(p, sm, pl, c * 8, toff, stage, cur);
+        V cur = TreeSum<T, 3>::run(p, sm, pl, c * 8, toff, stage);
         if (!(c & 1)) {
-#pragma unroll
-            for (int k = 0; k < U; ++k) s0[k] = cur[k];
+            s0 = cur;
             continue;
         }
-#pragma unroll
-        for (int k = 0; k < U; ++k) cur[k] = vadd(s0[k], cur[k]);
+        cur = vadd(s0, cur);
         if (!(c & 2)) {
-#pragma unroll
-            for (int k = 0; k < U; ++k) s1[k] = cur[k];
+            s1 = cur;
             continue;
         }
-#pragma unroll
-        for (int k = 0; k < U; ++k) cur[k] = vadd(s1[k], cur[k]);
+        cur = vadd(s1, cur);
         if (!(c & 4)) {
-#pragma unroll
-            for (int k = 0; k < U; ++k) s2[k] = cur[k];
+            s2 = cur;
             continue;
         }
-#pragma unroll
-        for (int k = 0; k < U; ++k) s3[k] = vadd(s2[k], cur[k]);
+        s3 = vadd(s2, cur);
     }
-#pragma unroll
-    for (int k = 0; k < U; ++k) out[k] = log_leaves == 4 ? s1[k] : (log_leaves == 5 ? s2[k] : s3[k]);
+    return log_leaves == 4 ? s1 : (log_leaves == 5 ? s2 : s3);
 }
 
 template <typename T>
-__device__ __forceinline__ void tree_sum(const LaunchParams& p, const SmemCtl& sm, int pl, int log_leaves,
-                                         int64_t toff, const typename Tr<T>::V* stage, typename Tr<T>::V* out) {
+__device__ __forceinline__ typename Tr<T>::V tree_sum(const LaunchParams& p, const SmemCtl& sm, int pl,
+                                                      int log_leaves, int64_t toff, const typename Tr<T>::V* stage) {
     switch (log_leaves) {
-        case 0: TreeSum<T, 0>::run(p, sm, pl, 0, toff, stage, out); break;
-        case 1: TreeSum<T, 1>::run(p, sm, pl, 0, toff, stage, out); break;
-        case 2: TreeSum<T, 2>::run(p, sm, pl, 0, toff, stage, out); break;
-        case 3: TreeSum<T, 3>::run(p, sm, pl, 0, toff, stage, out); break;
-        default: tree_sum_big<T>(p, sm, pl, log_leaves, toff, stage, out); break;
+        case 0: return TreeSum<T, 0>::run(p, sm, pl, 0, toff, stage);
+        case 1: return TreeSum<T, 1>::run(p, sm, pl, 0, toff, stage);
+        case 2: return TreeSum<T, 2>::run(p, sm, pl, 0, toff, stage);
+        case 3: return TreeSum<T, 3>::run(p, sm, pl, 0, toff, stage);
+        default: return tree_sum_big<T>(p, sm, pl, log_leaves, toff, stage);
     }
 }
 
@@ -811,32 +806,22 @@ __device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, c
             if (poll_cycles) *poll_cycles += clock64() - c0;
             if (__any_sync(0xffffffffu, rc != 0) || sm.abort) return false;
         }
-        V acc[U];
-        tree_sum<T>(p, sm, pl, P_.log_leaves, tbase, stage, acc);
+        const V acc = tree_sum<T>(p, sm, pl, P_.log_leaves, tbase, stage);
         // timely members share one result: acc/S or total/P (optim.py:442,452);
         // a power-of-two divisor is an exact reciprocal multiply (same IEEE result)
-        V avg[U];
-        const T inv = T(1) / T(P_.divisor);
-#pragma unroll
-        for (int k = 0; k < U; ++k) avg[k] = P_.divisor_pow2 ? vscale(inv, acc[k]) : vdiv(acc[k], T(P_.divisor));
+        const V avg = P_.divisor_pow2 ? vscale(T(1) / T(P_.divisor), acc) : vdiv(acc, T(P_.divisor));
+        const int64_t idx = tbase + int64_t(tid) * E;
         for (int mi = 0; mi < P_.n_members; ++mi) {
             const int j = P_.members[mi];
             const DevJob& jb = p.jobs[j];
             if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
-                T* out = static_cast<T*>(jb.acc_out);
-#pragma unroll
-                for (int k = 0; k < U; ++k) st_stream<T>(out, tbase + int64_t(k * kThreads + tid) * E, p.n, acc[k]);
+                st_stream<T>(static_cast<T*>(jb.acc_out), idx, p.n, acc);
                 continue;
             }
-            T* W = static_cast<T*>(jb.W);
             const bool timely = jb.kind == WG_JOB_SYNC_STEP || sm.stamps[jb.vidx][jb.rank] == jb.version;
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                // late member: (acc + W')/(S+1)  (optim.py:443-444), true IEEE division
-                const V out = timely ? avg[k] : vdiv(vadd(acc[k], stage[(j * U + k) * kThreads + tid]),
-                                                     T(P_.divisor + 1));
-                st_stream<T>(W, tbase + int64_t(k * kThreads + tid) * E, p.n, out);
-            }
+            // late member: (acc + W')/(S+1)  (optim.py:443-444), true IEEE division
+            const V out = timely ? avg : vdiv(vadd(acc, stage[j * kThreads + tid]), T(P_.divisor + 1));
+            st_stream<T>(static_cast<T*>(jb.W), idx, p.n, out);
         }
     }
     return true;
@@ -907,75 +892,38 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
             p.prof[blockIdx.x * 8 + 5] = my_tiles;
         }
     } else {
-    const int J = p.n_jobs;
-    V* ring = stage;  // [kDepth][3][kThreads]
-    V* stages[2] = {ring + kDepth * 3 * kThreads, ring + kDepth * 3 * kThreads + size_t(J) * kThreads};
-    const int64_t my_ntiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int64_t n_items = my_ntiles * J;
-    const bool prof = AHEAD && p.prof != nullptr && threadIdx.x == 0;
-    long long cyc[6] = {0, 0, 0, 0, 0, 0};
-    long long c0 = prof ? clock64() : 0;
-    auto lap = [&](int i) {
-        if (prof) {
-            const long long c = clock64();
-            cyc[i] += c - c0;
-            c0 = c;
-        }
-    };
-    auto item_tile = [&](int64_t i) { return int64_t(blockIdx.x) + (i / J) * int64_t(gridDim.x); };
+        // one GPU: nobody outside this CTA waits for its tiles
+        const int J = p.n_jobs;
+        V* ring = stage;  // [kDepth][3][kThreads], then the W' stage [J][kThreads]
+        V* st = ring + kDepth * 3 * kThreads;
+        const int64_t my_ntiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+        const int64_t n_items = my_ntiles * J;
 #pragma unroll
-    for (int d = 0; d < kDepth; ++d) {
-        if (d < n_items) issue_item<T>(p, item_tile(d), int(d % J), ring + d * 3 * kThreads);
-        cp_async_commit();
-    }
-    int64_t i = 0;
-    bool ok = true;
-    for (int64_t kk = 0; kk < my_ntiles && ok; ++kk) {
-        const int64_t tile = int64_t(blockIdx.x) + kk * gridDim.x;
-        V* st = stages[AHEAD ? (kk & 1) : 0];
-        for (int j = 0; j < J; ++j, ++i) {
-            cp_async_wait<kDepth - 1>();
-            V* slot = ring + (i % kDepth) * 3 * kThreads;
-            compute_item<T>(p, tile, j, slot, st);
-            if (i + kDepth < n_items) issue_item<T>(p, item_tile(i + kDepth), int((i + kDepth) % J), slot);
+        for (int d = 0; d < kDepth; ++d) {
+            if (d < n_items)
+                issue_item<T>(p, int64_t(blockIdx.x) + (d / J) * int64_t(gridDim.x), d % J, ring + d * 3 * kThreads);
             cp_async_commit();
         }
-        ++my_tiles;
-        lap(0);
-        if (AHEAD) {
-            // peers pull our tiles: publish now, consume the previous tile so
-            // a flag is out a whole tile before the mirroring peer CTA needs it
-            publish_tile(p, tile);
-            lap(1);
-            if (kk == 0) continue;
-        }
-        if (!resolved) {
-            if (!resolve_sources<T>(p, sm)) {
-                ok = false;
-                break;
+        int64_t i = 0;
+        for (int64_t kk = 0; kk < my_ntiles; ++kk) {
+            const int64_t tile = int64_t(blockIdx.x) + kk * gridDim.x;
+            for (int j = 0; j < J; ++j, ++i) {
+                cp_async_wait<kDepth - 1>();
+                V* slot = ring + (i % kDepth) * 3 * kThreads;
+                compute_item<T>(p, tile, j, slot, st);
+                const int64_t nx = i + kDepth;
+                if (nx < n_items)
+                    issue_item<T>(p, int64_t(blockIdx.x) + (nx / J) * int64_t(gridDim.x), int(nx % J), slot);
+                cp_async_commit();
             }
-            resolved = true;
-            lap(2);
+            ++my_tiles;
+            if (!resolved) {
+                if (!resolve_sources<T>(p, sm)) break;
+                resolved = true;
+            }
+            if (!consume_tile<T>(p, sm, tile, st)) break;
         }
-        const int64_t ctile = AHEAD ? tile - gridDim.x : tile;
-        V* cst = AHEAD ? stages[(kk - 1) & 1] : st;
-        if (!consume_tile<T>(p, sm, ctile, cst, prof ? &cyc[3] : nullptr)) ok = false;
-        lap(4);
-    }
-    if (AHEAD && ok && my_ntiles > 0) {
-        if (!resolved) resolved = resolve_sources<T>(p, sm);
-        if (resolved) {
-            const int64_t last = int64_t(blockIdx.x) + (my_ntiles - 1) * gridDim.x;
-            consume_tile<T>(p, sm, last, stages[(my_ntiles - 1) & 1], prof ? &cyc[3] : nullptr);
-            lap(4);
-        }
-    }
-    cp_async_wait<0>();
-    if (prof) {
-        cyc[4] -= cyc[3];
-        for (int q = 0; q < 5; ++q) p.prof[blockIdx.x * 8 + q] = cyc[q];
-        p.prof[blockIdx.x * 8 + 5] = my_tiles;
-    }
+        cp_async_wait<0>();
     }
     publish_slots(p, sm.abort ? 0u : my_tiles);
     if (blockIdx.x == 0) {
