@@ -45,10 +45,10 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference", "nccl"])
     ap.add_argument("--P", type=int, default=8)
     ap.add_argument("--S", type=int, default=8)
-    ap.add_argument("--n", type=int, default=N_RESNET50)
+    ap.add_argument("--nparams", type=int, default=N_RESNET50, dest="n")
     ap.add_argument("--tau", type=int, default=10)
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps (capped at 60)")
@@ -242,6 +242,7 @@ def run_ours(a):
     import torch.distributed as dist
 
     from paper_2005_00124_b200.context import DeviceContext
+    from paper_2005_00124_b200.dist import max_over_ranks
     from paper_2005_00124_b200.optim import EtaSchedule, GroupAveragingOptimizer, OptimizerConfig
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -264,11 +265,7 @@ def run_ours(a):
             dist.barrier()
 
     def allmax(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return max_over_ranks(x, device=dev)
 
     ctx = DeviceContext(a.P, a.S, a.n, dtype=dt, tau=a.tau, n_gpus=G, gpu_index=rank, device=dev.index,
                         grace_us=a.grace_us, timeout_s=30.0)
@@ -389,10 +386,89 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# NCCL sub-communicator baseline (comparison only; one WAGMA rank per GPU)
+# ---------------------------------------------------------------------------
+
+def run_nccl(a):
+    """torch momentum step + ncclAllReduce(AVG) on per-group sub-communicators.
+
+    Blocking (beta) semantics: every rank waits for its whole group. One rank
+    per GPU (NCCL cannot host several ranks of a communicator on one GPU), so
+    P = world size; groups come from the same schedule (compute_groups), one
+    communicator per distinct group of the schedule period (ncclCommSplit via
+    torch.distributed.new_group), the global sync every tau iterations.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_00124_b200.dist import max_over_ranks
+    from paper_2005_00124_b200.topology import GroupingParams, compute_groups
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P, S = world, min(a.S, world)
+    dt = torch.float32 if a.dtype == "f32" else torch.float64
+    period = max(1, (P.bit_length() - 1)) if P > 1 else 1
+    comms = {}
+    for t in range(period):
+        for grp in compute_groups(GroupingParams(P, S, t)).groups:
+            if grp not in comms and len(grp) > 1:
+                comms[grp] = dist.new_group(list(grp)) if world > 1 else None
+    gen = torch.Generator(device=dev).manual_seed(1234)
+    W = torch.randn(a.n, generator=gen, device=dev, dtype=dt) * 0.02
+    m = torch.zeros_like(W)
+    gpool = [torch.randn(a.n, generator=gen, device=dev, dtype=dt) * 0.01 for _ in range(2)]
+
+    def step(t):
+        m.mul_(0.9).add_(gpool[t % 2])
+        W.sub_(m, alpha=0.1)
+        if world == 1:
+            return
+        if (t + 1) % a.tau == 0:
+            dist.all_reduce(W, op=dist.ReduceOp.AVG)
+        else:
+            grp = compute_groups(GroupingParams(P, S, t)).group_of(rank)
+            if len(grp) > 1:
+                dist.all_reduce(W, op=dist.ReduceOp.AVG, group=comms[grp])
+
+    for t in range(a.warmup):
+        step(t)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for t in range(a.warmup, a.warmup + a.steps):
+        step(t)
+    s1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(s0.elapsed_time(s1), device=dev) / a.steps
+    if rank == 0:
+        elem = 4 if a.dtype == "f32" else 8
+        busbw = 2 * (S - 1) / S * elem * a.n / (ms / 1e3) / 1e9 if S > 1 else 0.0
+        cfg = config_dict(a, world)
+        cfg.update({"ranks": P, "group_size": S, "rank_mapping": "one rank per GPU",
+                    "parallelism": f"nccl-subcomm-p{P}-g{world}", "activation": "blocking (beta)"})
+        print(json.dumps({"metric": METRIC, "value": 1000.0 / ms, "unit": "iters/s", "impl": "nccl",
+                          "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": a.dtype,
+                          "data": "synthetic", "config": cfg, "nccl_busbw_gbs": busbw}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.impl == "nccl":
+        run_nccl(a)
     else:
         run_ours(a)
 

@@ -115,7 +115,8 @@ class DeviceContext:
         if self.P % self.n_gpus:
             raise InvalidParamsError(f"n_gpus={n_gpus} must divide P={P}")
         self.R = self.P // self.n_gpus
-        self.local_ranks = range(self.gpu_index * self.R, (self.gpu_index + 1) * self.R)
+        from .dist import rank_layout
+        self.local_ranks = rank_layout(self.P, self.n_gpus, self.gpu_index)
         cfg = _lib.WgConfig()
         cfg.P, cfg.S, cfg.n_gpus, cfg.gpu_index, cfg.device = self.P, self.S, self.n_gpus, self.gpu_index, self.device
         cfg.dtype = _dtype_code(dtype)
@@ -181,9 +182,12 @@ class DeviceContext:
 
     def _exchange_handles(self, process_group) -> None:
         import torch.distributed as dist
-        blobs: list = [None] * dist.get_world_size(process_group)
-        dist.all_gather_object(blobs, (self.gpu_index, self.export_blob()), group=process_group)
-        for gi, blob in blobs:
+
+        from .dist import exchange_blobs
+        blobs = exchange_blobs(self.gpu_index, self.export_blob(), process_group)
+        if sorted(blobs) != list(range(self.n_gpus)):
+            raise RuntimeError(f"expected blobs from gpus 0..{self.n_gpus - 1}, got {sorted(blobs)}")
+        for gi, blob in blobs.items():
             if gi != self.gpu_index:
                 self.import_blob(gi, blob)
         dist.barrier(group=process_group)

@@ -129,8 +129,8 @@ struct LaunchParams {
     int64_t forced[kMaxVersions][kMaxP];
     wg_job_status* status;
     long long* prof;  // optional per-CTA phase cycle counters [grid][8]
-    int32_t fence_scope;  // 0 sys (default), 1 gpu, 2 none (timing experiments only)
-    int32_t pad2;
+    int32_t fence_scope;  // 0 sys, 1 gpu (default), 2 none (timing experiments only)
+    int32_t nvl_stages;   // leaf-ring stages of the multi-GPU TMA kernel
 };
 
 // ---------------------------------------------------------------------------
@@ -422,10 +422,11 @@ struct SmemCtl {
     int32_t abort;
 };
 
-// Resolve every plan's leaves to a source once per CTA (after lock-in).
-template <typename T>
-__device__ bool resolve_sources(const LaunchParams& p, SmemCtl& sm) {
-    const int tid = threadIdx.x;
+// Resolve every plan's leaves to a source (after lock-in), executed by
+// `nthr` threads starting at thread index `t0` (the whole CTA, or one warp)
+// separated by `sync()`.
+template <typename T, class Sync>
+__device__ bool resolve_core(const LaunchParams& p, SmemCtl& sm, int tid, int nthr, Sync sync) {
     const uint64_t t0 = globaltimer();
     if (tid == 0) {
         for (int vi = 0; vi < p.n_versions && !sm.abort; ++vi) {
@@ -438,9 +439,9 @@ __device__ bool resolve_sources(const LaunchParams& p, SmemCtl& sm) {
             }
         }
     }
-    __syncthreads();
+    sync();
     if (sm.abort) return false;
-    for (int i = tid; i < p.n_versions * p.P; i += blockDim.x) {
+    for (int i = tid; i < p.n_versions * p.P; i += nthr) {
         const int vi = i / p.P, q = i % p.P;
         const DevVersion& dv = p.versions[vi];
         int64_t s;
@@ -452,8 +453,8 @@ __device__ bool resolve_sources(const LaunchParams& p, SmemCtl& sm) {
             s = dv.version;
         sm.stamps[vi][q] = s;
     }
-    __syncthreads();
-    for (int i = tid; i < p.n_plans * kMaxLeaves; i += blockDim.x) {
+    sync();
+    for (int i = tid; i < p.n_plans * kMaxLeaves; i += nthr) {
         const int pl = i / kMaxLeaves, li = i % kMaxLeaves;
         const DevPlan& P_ = p.plans[pl];
         if (li >= P_.n_leaves) continue;
@@ -483,14 +484,19 @@ __device__ bool resolve_sources(const LaunchParams& p, SmemCtl& sm) {
         }
         sm.leaf_src[pl][li] = src;
     }
-    __syncthreads();
+    sync();
     if (tid < p.n_plans) {
         int polls = 0;
         for (int li = 0; li < p.plans[tid].n_leaves; ++li) polls |= (sm.leaf_src[tid][li] == kSrcPoll);
         sm.plan_polls[tid] = polls;
     }
-    __syncthreads();
+    sync();
     return !sm.abort;
+}
+
+template <typename T>
+__device__ bool resolve_sources(const LaunchParams& p, SmemCtl& sm) {
+    return resolve_core<T>(p, sm, threadIdx.x, blockDim.x, [] { __syncthreads(); });
 }
 
 // ---------------------------------------------------------------------------
@@ -539,7 +545,7 @@ __device__ __forceinline__ void issue_item(const LaunchParams& p, int64_t tile, 
 
 // Local step of one item + send-ring install + stage (optim.py:176-183,
 // collective.py:95-101).
-template <typename T>
+template <typename T, bool STAGE = true>
 __device__ __forceinline__ void compute_item(const LaunchParams& p, int64_t tile, int j,
                                              const typename Tr<T>::V* slot, typename Tr<T>::V* stage) {
     using V = typename Tr<T>::V;
@@ -569,7 +575,7 @@ __device__ __forceinline__ void compute_item(const LaunchParams& p, int64_t tile
     }
     // SendBuffer.install: W' written once into the send ring, and staged
     __stcg(reinterpret_cast<V*>(ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + idx), wp);
-    stage[j * kThreads + tid] = wp;
+    if (STAGE) stage[j * kThreads + tid] = wp;
 }
 
 // Multi-GPU kernel: register-pipelined produce (the next job's loads in
@@ -708,42 +714,35 @@ __device__ __forceinline__ void publish_slots(const LaunchParams& p, unsigned my
 
 static_assert(kVecPerThread == 1, "the consume path is written for one 16-byte vector per thread");
 
+// Butterfly tree over leaves [leaf0, leaf0 + 2^LOG): level r adds the
+// subtrees that differ in bit r of the leaf index (collective.py:310-329).
+// `fetch(leaf)` returns this thread's vector of a leaf.
 template <typename T, int LOG>
 struct TreeSum {
-    using V = typename Tr<T>::V;
-    static __device__ __forceinline__ V run(const LaunchParams& p, const SmemCtl& sm, int pl, int leaf0,
-                                            int64_t toff, const V* stage) {
-        const V a = TreeSum<T, LOG - 1>::run(p, sm, pl, leaf0, toff, stage);
-        const V b = TreeSum<T, LOG - 1>::run(p, sm, pl, leaf0 + (1 << (LOG - 1)), toff, stage);
+    template <class F>
+    static __device__ __forceinline__ typename Tr<T>::V run(const F& fetch, int leaf0) {
+        const auto a = TreeSum<T, LOG - 1>::run(fetch, leaf0);
+        const auto b = TreeSum<T, LOG - 1>::run(fetch, leaf0 + (1 << (LOG - 1)));
         return vadd(a, b);
     }
 };
 template <typename T>
 struct TreeSum<T, 0> {
-    using V = typename Tr<T>::V;
-    static __device__ __forceinline__ V run(const LaunchParams& p, const SmemCtl& sm, int pl, int leaf,
-                                            int64_t toff, const V* stage) {
-        constexpr int E = Tr<T>::EPV;
-        const int src = sm.leaf_src[pl][leaf];
-        const int tid = threadIdx.x;
-        if (src >= 0) return stage[src * kThreads + tid];
-        // 128-bit load of a peer's (NVLink) or an older local send slot;
-        // .cg: L2 only, never a stale L1 line of a re-published slot.
-        const T* base = ring_ptr<T>(p, p.plans[pl].leaves[leaf], sm.leaf_slot[pl][leaf]) + toff;
-        return __ldcg(reinterpret_cast<const V*>(base + int64_t(tid) * E));
+    template <class F>
+    static __device__ __forceinline__ typename Tr<T>::V run(const F& fetch, int leaf) {
+        return fetch(leaf);
     }
 };
 
 // Trees of 16..64 leaves: 8-leaf subtrees combined through a 4-level
 // register stack (static indices only), same pairing as the full tree.
-template <typename T>
-__device__ __noinline__ typename Tr<T>::V tree_sum_big(const LaunchParams& p, const SmemCtl& sm, int pl,
-                                                       int log_leaves, int64_t toff, const typename Tr<T>::V* stage) {
+template <typename T, class F>
+__device__ __forceinline__ typename Tr<T>::V tree_sum_big(const F& fetch, int log_leaves) {
     using V = typename Tr<T>::V;
     V s0, s1, s2, s3;
     const int nchunks = 1 << (log_leaves - 3);
     for (int c = 0; c < nchunks; ++c) {
-        V cur = TreeSum<T, 3>::run(p, sm, pl, c * 8, toff, stage);
+        V cur = TreeSum<T, 3>::run(fetch, c * 8);
         if (!(c & 1)) {
             s0 = cur;
             continue;
@@ -763,15 +762,37 @@ __device__ __noinline__ typename Tr<T>::V tree_sum_big(const LaunchParams& p, co
     return log_leaves == 4 ? s1 : (log_leaves == 5 ? s2 : s3);
 }
 
-template <typename T>
-__device__ __forceinline__ typename Tr<T>::V tree_sum(const LaunchParams& p, const SmemCtl& sm, int pl,
-                                                      int log_leaves, int64_t toff, const typename Tr<T>::V* stage) {
+template <typename T, class F>
+__device__ __forceinline__ typename Tr<T>::V tree_sum(const F& fetch, int log_leaves) {
     switch (log_leaves) {
-        case 0: return TreeSum<T, 0>::run(p, sm, pl, 0, toff, stage);
-        case 1: return TreeSum<T, 1>::run(p, sm, pl, 0, toff, stage);
-        case 2: return TreeSum<T, 2>::run(p, sm, pl, 0, toff, stage);
-        case 3: return TreeSum<T, 3>::run(p, sm, pl, 0, toff, stage);
-        default: return tree_sum_big<T>(p, sm, pl, log_leaves, toff, stage);
+        case 0: return TreeSum<T, 0>::run(fetch, 0);
+        case 1: return TreeSum<T, 1>::run(fetch, 0);
+        case 2: return TreeSum<T, 2>::run(fetch, 0);
+        case 3: return TreeSum<T, 3>::run(fetch, 0);
+        default: return tree_sum_big<T>(fetch, log_leaves);
+    }
+}
+
+// Averaging rule for every member of a plan (optim.py:439-452) given its sum.
+// `own_wp(j)` returns this thread's W' of job j (only read for late members).
+template <typename T, class OwnWp>
+__device__ __forceinline__ void finish_members(const LaunchParams& p, const SmemCtl& sm, const DevPlan& P_,
+                                               typename Tr<T>::V acc, int64_t idx, const OwnWp& own_wp) {
+    using V = typename Tr<T>::V;
+    // timely members share one result: acc/S or total/P (optim.py:442,452);
+    // a power-of-two divisor is an exact reciprocal multiply (same IEEE result)
+    const V avg = P_.divisor_pow2 ? vscale(T(1) / T(P_.divisor), acc) : vdiv(acc, T(P_.divisor));
+    for (int mi = 0; mi < P_.n_members; ++mi) {
+        const int j = P_.members[mi];
+        const DevJob& jb = p.jobs[j];
+        if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
+            st_stream<T>(static_cast<T*>(jb.acc_out), idx, p.n, acc);
+            continue;
+        }
+        const bool timely = jb.kind == WG_JOB_SYNC_STEP || sm.stamps[jb.vidx][jb.rank] == jb.version;
+        // late member: (acc + W')/(S+1)  (optim.py:443-444), true IEEE division
+        const V out = timely ? avg : vdiv(vadd(acc, own_wp(j)), T(P_.divisor + 1));
+        st_stream<T>(static_cast<T*>(jb.W), idx, p.n, out);
     }
 }
 
@@ -806,23 +827,16 @@ __device__ bool consume_tile(const LaunchParams& p, SmemCtl& sm, int64_t tile, c
             if (poll_cycles) *poll_cycles += clock64() - c0;
             if (__any_sync(0xffffffffu, rc != 0) || sm.abort) return false;
         }
-        const V acc = tree_sum<T>(p, sm, pl, P_.log_leaves, tbase, stage);
-        // timely members share one result: acc/S or total/P (optim.py:442,452);
-        // a power-of-two divisor is an exact reciprocal multiply (same IEEE result)
-        const V avg = P_.divisor_pow2 ? vscale(T(1) / T(P_.divisor), acc) : vdiv(acc, T(P_.divisor));
-        const int64_t idx = tbase + int64_t(tid) * E;
-        for (int mi = 0; mi < P_.n_members; ++mi) {
-            const int j = P_.members[mi];
-            const DevJob& jb = p.jobs[j];
-            if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
-                st_stream<T>(static_cast<T*>(jb.acc_out), idx, p.n, acc);
-                continue;
-            }
-            const bool timely = jb.kind == WG_JOB_SYNC_STEP || sm.stamps[jb.vidx][jb.rank] == jb.version;
-            // late member: (acc + W')/(S+1)  (optim.py:443-444), true IEEE division
-            const V out = timely ? avg : vdiv(vadd(acc, stage[j * kThreads + tid]), T(P_.divisor + 1));
-            st_stream<T>(static_cast<T*>(jb.W), idx, p.n, out);
-        }
+        auto fetch = [&](int leaf) -> V {
+            const int src = sm.leaf_src[pl][leaf];
+            if (src >= 0) return stage[src * kThreads + tid];
+            // 128-bit load of a peer's (NVLink) or an older local send slot;
+            // .cg: L2 only, never a stale L1 line of a re-published slot.
+            const T* base = ring_ptr<T>(p, P_.leaves[leaf], sm.leaf_slot[pl][leaf]) + tbase;
+            return __ldcg(reinterpret_cast<const V*>(base + int64_t(tid) * E));
+        };
+        finish_members<T>(p, sm, P_, tree_sum<T>(fetch, P_.log_leaves), tbase + int64_t(tid) * E,
+                          [&](int j) { return stage[j * kThreads + tid]; });
     }
     return true;
 }
@@ -943,6 +957,396 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
     }
 }
 
+// ---------------------------------------------------------------------------
+// multi-GPU kernel: producer / puller / consumer warps
+//
+//  - 8 producer warps stream W, g, m through a per-thread cp.async ring, do the
+//    local step, install W' in the send ring and publish a per-warp flag per
+//    tile; they never wait on anything else, so they run ahead of the pulls.
+//  - 1 puller warp walks the same tiles: waits for every leaf's flag (peer
+//    GPUs over NVLink, and this GPU's own producers), then fetches each
+//    leaf-tile with one TMA bulk copy (cp.async.bulk global->shared; peer
+//    memory is read over NVLink) into a deep shared-memory ring whose stages
+//    are guarded by mbarriers (full: TMA bytes landed; empty: consumed).
+//  - 8 consumer warps sum the leaves of each plan from shared memory in the
+//    butterfly order and write W_{t+1}.
+// One 544-thread CTA per SM; stage count chosen from the shared-memory budget.
+// ---------------------------------------------------------------------------
+
+#ifndef WG_NVL_DEPTH
+#define WG_NVL_DEPTH 3
+#endif
+#ifndef WG_NVL_TMA_LOCAL
+#define WG_NVL_TMA_LOCAL 1
+#endif
+constexpr int kNvlDepth = WG_NVL_DEPTH;  // producer cp.async ring depth (items)
+constexpr int kNvlMaxStages = 16;
+constexpr int kNvlThreads = 2 * kThreads + 32;
+constexpr int kNvlMaxDyn = 200 * 1024;
+constexpr int kPollPerLane = 8;
+constexpr int kPullBatch = 8;  // tiles whose flags are polled and copies issued together
+constexpr int kPubChunk = 8;   // tiles published together (one fence per chunk)
+constexpr int kPubRing = 16;   // per-chunk producer-completion counters (drift bound kPubRing/2 chunks)
+constexpr int kMaxPoll = 32 * kPollPerLane;  // (leaf, warp) flags polled per tile
+
+__device__ __forceinline__ unsigned smem_u32(const void* ptr) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n selp.u32 %0, 1, 0, q;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Wait for an mbarrier phase with the watchdog; false on timeout / abort.
+__device__ bool mbar_wait(const LaunchParams& p, uint64_t* bar, unsigned parity) {
+    uint64_t t0 = 0;
+    int it = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if ((++it & 255) == 0) {
+            if (t0 == 0) {
+                t0 = globaltimer();
+            } else if (globaltimer() - t0 > uint64_t(p.timeout_ns)) {
+                return false;
+            }
+            if (aborted(p)) return false;
+        }
+    }
+    return true;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_constant__ LaunchParams p) {
+    using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
+    extern __shared__ __align__(128) unsigned char dyn_smem[];
+    __shared__ SmemCtl sm;
+    __shared__ __align__(8) uint64_t full[kNvlMaxStages];
+    __shared__ __align__(8) uint64_t empty[kNvlMaxStages];
+    __shared__ int leaf_base[kMaxPlans + 1];
+    __shared__ volatile int ready;
+    __shared__ int16_t poll_q[kMaxPoll];
+    __shared__ int8_t poll_w[kMaxPoll];
+    __shared__ int64_t poll_s[kMaxPoll];
+    __shared__ int n_poll_sh;
+    __shared__ int n_rows_sh;
+    __shared__ unsigned pub_count[kPubRing];
+    __shared__ int8_t tma_row[kMaxPlans * kMaxLeaves];  // flat leaf -> row of the TMA ring (-1: read from global)
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int J = p.n_jobs;
+    const int NS = p.nvl_stages;
+    if (tid == 0) {
+        sm.abort = 0;
+        ready = 0;
+        for (int st = 0; st < NS; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], kWarps);
+        }
+        int acc = 0, nr = 0;
+        for (int pl = 0; pl < p.n_plans; ++pl) {
+            leaf_base[pl] = acc;
+            for (int li = 0; li < p.plans[pl].n_leaves; ++li)
+                tma_row[acc + li] =
+                    (WG_NVL_TMA_LOCAL || p.plans[pl].leaves[li] / p.R != p.gpu_index) ? int8_t(nr++) : int8_t(-1);
+            acc += p.plans[pl].n_leaves;
+        }
+        leaf_base[p.n_plans] = acc;
+        n_rows_sh = nr;
+    }
+    if (tid < kMaxVersions) sm.activator[tid] = 0;
+    if (tid < kPubRing) pub_count[tid] = 0;
+    __syncthreads();
+    const int NL = leaf_base[p.n_plans];
+    const int NR = n_rows_sh;  // leaves on other GPUs: fetched by TMA over NVLink
+    V* leafbuf = reinterpret_cast<V*>(dyn_smem);          // [NS][NR][kThreads]
+    V* ring = leafbuf + size_t(NS) * NR * kThreads;         // [kNvlDepth][3][kThreads]
+    const int64_t my_ntiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const unsigned tile_bytes = unsigned(p.tile_elems * int64_t(sizeof(T)));
+    unsigned my_tiles = 0;
+
+    if (warp < kWarps) {
+        // ---------------- producers ----------------
+        const int64_t n_items = my_ntiles * J;
+#pragma unroll
+        for (int d = 0; d < kNvlDepth; ++d) {
+            if (d < n_items)
+                issue_item<T>(p, int64_t(blockIdx.x) + (d / J) * int64_t(gridDim.x), d % J, ring + d * 3 * kThreads);
+            cp_async_commit();
+        }
+        int64_t i = 0;
+        const long long pc0 = clock64();
+        for (int64_t kk = 0; kk < my_ntiles; ++kk) {
+            const int64_t tile = int64_t(blockIdx.x) + kk * gridDim.x;
+            for (int j = 0; j < J; ++j, ++i) {
+                cp_async_wait<kNvlDepth - 1>();
+                V* slot = ring + (i % kNvlDepth) * 3 * kThreads;
+                compute_item<T, false>(p, tile, j, slot, nullptr);
+                const int64_t nx = i + kNvlDepth;
+                if (nx < n_items)
+                    issue_item<T>(p, int64_t(blockIdx.x) + (nx / J) * int64_t(gridDim.x), int(nx % J), slot);
+                cp_async_commit();
+            }
+            // Tiles are published in chunks of kPubChunk: the last producer
+            // warp to finish a chunk issues one GPU-scope fence (cumulative
+            // over the other warps' stores, acquired through the shared-memory
+            // counter) and writes the chunk's per-warp flags with all lanes.
+            // No other warp ever waits on a fence.
+            const bool chunk_end = ((kk + 1) % kPubChunk == 0) || (kk + 1 == my_ntiles);
+            if (chunk_end) {
+                __syncwarp();
+                unsigned old = 0;
+                if (lane == 0) {
+                    unsigned* cnt = &pub_count[(kk / kPubChunk) & (kPubRing - 1)];
+                    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                                 : "=r"(old)
+                                 : "r"(smem_u32(cnt))
+                                 : "memory");
+                    if (old == kWarps - 1) *cnt = 0;
+                }
+                old = __shfl_sync(0xffffffffu, old, 0);
+                if (old == kWarps - 1) {
+                    if (p.fence_scope == 0)
+                        fence_sys();
+                    else if (p.fence_scope == 1)
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    const int64_t k0 = kk - (kk % kPubChunk);
+                    const int nk = int(kk - k0 + 1);
+                    for (int e = lane; e < nk * J * kWarps; e += 32) {
+                        const int w = e % kWarps, j = (e / kWarps) % J, b = e / (kWarps * J);
+                        const DevJob& jb = p.jobs[j];
+                        if (jb.produces)
+                            st_relaxed_sys(flag_ptr(p, jb.rank, int64_t(blockIdx.x) + (k0 + b) * gridDim.x, w),
+                                           jb.version);
+                    }
+                }
+            }
+            ++my_tiles;
+            // bound the drift between producer warps (the counter ring)
+            if ((kk + 1) % (kPubChunk * kPubRing / 2) == 0) {
+                // named barrier over the 8 producer warps, OR-reducing the abort
+                // flag so that all of them leave together
+                int stop;
+                asm volatile(
+                    "{\n .reg .pred a, b;\n setp.ne.s32 a, %1, 0;\n bar.red.or.pred b, 1, %2, a;\n"
+                    " selp.s32 %0, 1, 0, b;\n}\n"
+                    : "=r"(stop)
+                    : "r"(int(aborted(p))), "n"(kThreads)
+                    : "memory");
+                if (stop) break;
+            }
+        }
+        cp_async_wait<0>();
+        if (p.prof && tid == 0) p.prof[blockIdx.x * 8 + 0] = clock64() - pc0;
+    } else if (warp == 2 * kWarps) {
+        // ---------------- puller ----------------
+        if (blockIdx.x == 0) control_phase(p, sm.activator);
+        bool resolved = resolve_core<T>(p, sm, lane, 32, [] { __syncwarp(); });
+        __syncwarp();
+        // every leaf goes through the ring; flags to wait for: peers'
+        // in-progress tiles and this GPU's own producers (this launch)
+        int n_poll = 0;
+        if (resolved && lane == 0) {
+            for (int pl = 0; pl < p.n_plans; ++pl)
+                for (int li = 0; li < p.plans[pl].n_leaves; ++li) {
+                    if (sm.leaf_src[pl][li] == kSrcReady) continue;
+                    const int q = p.plans[pl].leaves[li];
+                    if (sm.leaf_src[pl][li] >= 0) sm.leaf_slot[pl][li] = int16_t(slot_of(p, sm.stamps[p.plans[pl].vidx][q]));
+                    for (int w = 0; w < kWarps; ++w) {
+                        if (n_poll == kMaxPoll) {
+                            raise_error(p, WG_EINVAL, n_poll);
+                            break;
+                        }
+                        poll_q[n_poll] = int16_t(q);
+                        poll_w[n_poll] = int8_t(w);
+                        poll_s[n_poll] = sm.stamps[p.plans[pl].vidx][q];
+                        ++n_poll;
+                    }
+                }
+            n_poll_sh = n_poll;
+            __threadfence_block();
+            ready = aborted(p) ? 2 : 1;
+        } else if (!resolved && lane == 0) {
+            ready = 2;
+        }
+        __syncwarp();
+        resolved = resolved && ready == 1;
+        n_poll = n_poll_sh;
+        // Batches of up to kPullBatch tiles: one round of flag loads (all
+        // lanes, all tiles of the batch in flight), one acquire fence, then
+        // the TMA copies of the whole batch.
+        const int batch = NS - 1 < kPullBatch ? (NS > 1 ? NS - 1 : 1) : kPullBatch;
+        long long cy_empty = 0, cy_poll = 0, cy_issue = 0;
+        for (int64_t kc = 0; resolved && kc < my_ntiles; kc += batch) {
+            const int nb = int(my_ntiles - kc < batch ? my_ntiles - kc : batch);
+            bool ok = true;
+            long long c0 = clock64();
+            for (int b = 0; b < nb && ok; ++b) {
+                const int64_t k = kc + b;
+                if (k >= NS && !mbar_wait(p, &empty[k % NS], unsigned((k / NS - 1) & 1))) ok = false;
+            }
+            long long c1 = clock64();
+            cy_empty += c1 - c0;
+            if (!ok) {
+                if (lane == 0) raise_error(p, WG_ETIMEOUT, kc);
+                break;
+            }
+            int rc = 0;
+            const int total = nb * n_poll;
+            for (int base = 0; base < total && !rc; base += 32 * kPollPerLane) {
+                int64_t v[kPollPerLane];
+#pragma unroll
+                for (int r = 0; r < kPollPerLane; ++r) {  // issue the loads together
+                    const int e = base + lane + 32 * r;
+                    if (e < total) {
+                        const int idx = e % n_poll;
+                        const int64_t tile = int64_t(blockIdx.x) + (kc + e / n_poll) * gridDim.x;
+                        v[r] = ld_relaxed_sys(flag_ptr(p, poll_q[idx], tile, poll_w[idx]));
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < kPollPerLane; ++r) {
+                    const int e = base + lane + 32 * r;
+                    if (e >= total || rc) continue;
+                    const int idx = e % n_poll;
+                    const int64_t tile = int64_t(blockIdx.x) + (kc + e / n_poll) * gridDim.x;
+                    const uint64_t t0 = globaltimer();
+                    int it = 0;
+                    while (v[r] < poll_s[idx]) {
+                        if ((++it & 63) == 0 && (globaltimer() - t0 > uint64_t(p.timeout_ns) || aborted(p))) {
+                            rc = WG_ETIMEOUT;
+                            break;
+                        }
+                        __nanosleep(32);
+                        v[r] = ld_relaxed_sys(flag_ptr(p, poll_q[idx], tile, poll_w[idx]));
+                    }
+                    if (!rc && v[r] >= poll_s[idx] + p.D) rc = WG_EPROTO;
+                    if (rc) raise_error(p, rc, int64_t(poll_q[idx]) << 32 | (tile & 0xffffffff));
+                }
+            }
+            if (__any_sync(0xffffffffu, rc != 0)) break;
+            __syncwarp();
+            long long c2 = clock64();
+            cy_poll += c2 - c1;
+            // flags were read relaxed: acquire fence (GPU scope suffices: tile
+            // and flag are both read where they live, see publish_tile), then
+            // order it before the async-proxy (TMA) reads; every lane fences,
+            // then lane r issues the copies of TMA row r
+            if (p.fence_scope == 0)
+                fence_sys();
+            else
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            for (int b = 0; b < nb; ++b) {
+                const int64_t k = kc + b;
+                const int st = int(k % NS);
+                if (lane == 0) mbar_arrive_expect_tx(&full[st], unsigned(NR) * tile_bytes);
+            }
+            __syncwarp();
+            for (int e = lane; e < nb * NL; e += 32) {
+                const int b = e / NL, f = e % NL;
+                const int row = tma_row[f];
+                if (row < 0) continue;
+                int pl = 0;
+                while (leaf_base[pl + 1] <= f) ++pl;
+                const int li = f - leaf_base[pl];
+                const int64_t k = kc + b;
+                const int st = int(k % NS);
+                const int64_t tile = int64_t(blockIdx.x) + k * gridDim.x;
+                const T* src = ring_ptr<T>(p, p.plans[pl].leaves[li], sm.leaf_slot[pl][li]) + tile * p.tile_elems;
+                bulk_g2s(leafbuf + (size_t(st) * NR + row) * kThreads, src, tile_bytes, &full[st]);
+            }
+            __syncwarp();
+            cy_issue += clock64() - c2;
+        }
+        if (p.prof && lane == 0) {
+            p.prof[blockIdx.x * 8 + 1] = cy_empty;
+            p.prof[blockIdx.x * 8 + 2] = cy_poll;
+            p.prof[blockIdx.x * 8 + 3] = cy_issue;
+        }
+    } else {
+        // ---------------- consumers ----------------
+        const int ctid = tid - kThreads;  // vector index within the tile
+        const long long cc0 = clock64();
+        while (ready == 0) __nanosleep(64);
+        const long long cc1 = clock64();
+        long long cy_full = 0;
+        if (ready == 1) {
+            for (int64_t kc = 0; kc < my_ntiles; ++kc) {
+                const int st = int(kc % NS);
+                const long long w0 = clock64();
+                if (!mbar_wait(p, &full[st], unsigned((kc / NS) & 1))) {
+                    if (lane == 0) raise_error(p, WG_ETIMEOUT, kc);
+                    break;
+                }
+                cy_full += clock64() - w0;
+                const int64_t tile = int64_t(blockIdx.x) + kc * gridDim.x;
+                const int64_t idx = tile * p.tile_elems + int64_t(ctid) * E;
+                const V* lb = leafbuf + size_t(st) * NR * kThreads;
+                for (int pl = 0; pl < p.n_plans; ++pl) {
+                    const DevPlan& P_ = p.plans[pl];
+                    const int base = leaf_base[pl];
+                    auto fetch = [&](int leaf) -> V {
+                        const int row = tma_row[base + leaf];
+                        if (row >= 0) return lb[row * kThreads + ctid];
+                        // this GPU's leaf: the slot tile (published, usually in L2)
+                        return __ldcg(reinterpret_cast<const V*>(
+                            ring_ptr<T>(p, P_.leaves[leaf], sm.leaf_slot[pl][leaf]) + idx));
+                    };
+                    auto own_wp = [&](int j) -> V {
+                        const DevJob& jb = p.jobs[j];
+                        return __ldcg(reinterpret_cast<const V*>(ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + idx));
+                    };
+                    finish_members<T>(p, sm, P_, tree_sum<T>(fetch, P_.log_leaves), idx, own_wp);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+            }
+        }
+        if (p.prof && ctid == 0) {
+            p.prof[blockIdx.x * 8 + 4] = cy_full;
+            p.prof[blockIdx.x * 8 + 6] = clock64() - cc0;
+            p.prof[blockIdx.x * 8 + 7] = cc1 - cc0;
+        }
+    }
+    if (aborted(p)) sm.abort = 1;
+    publish_slots(p, sm.abort ? 0u : my_tiles);
+    if (blockIdx.x == 0) {
+        __syncthreads();
+        const bool res = ready == 1;
+        if (tid < p.n_jobs) {
+            const DevJob& jb = p.jobs[tid];
+            wg_job_status stt;
+            stt.version = jb.version;
+            stt.contrib_stamp = (jb.kind == WG_JOB_LOCAL_STEP || !res) ? jb.version : sm.stamps[jb.vidx][jb.rank];
+            stt.timely = stt.contrib_stamp == jb.version;
+            stt.activator = jb.vidx >= 0 ? sm.activator[jb.vidx] : 0;
+            stt.error = int32_t(ld_relaxed_sys(err_ptr(p)));
+            stt.pad = 0;
+            p.status[tid] = stt;
+        }
+    }
+}
+
 __global__ void fill_i64_kernel(int64_t* p, int64_t n, int64_t v) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) p[i] = v;
 }
@@ -995,6 +1399,8 @@ struct wg_ctx {
     int occ[2 * kMaxJobs + 1];
     long long* prof;
     int fence_scope;
+    int use_nvl;
+    int occ_nvl[2];
 };
 
 extern "C" {
@@ -1091,6 +1497,10 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
             e = cudaFuncSetAttribute(wagma_step_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(wagma_step_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(wagma_nvl_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNvlMaxDyn);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(wagma_nvl_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNvlMaxDyn);
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)); break; }
         e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, c.device);
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "device attribute: %s", cudaGetErrorString(e)); break; }
@@ -1103,6 +1513,8 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     }
     ctx->base[c.gpu_index] = ctx->arena;
     ctx->opened[c.gpu_index] = false;
+    ctx->use_nvl = 1;
+    if (const char* nv = getenv("WG_NVL")) ctx->use_nvl = atoi(nv);
     ctx->fence_scope = 1;  // GPU scope for per-tile flags (see publish_tile)
     if (const char* fs = getenv("WG_FENCE_SCOPE")) {
         if (!strcmp(fs, "sys")) ctx->fence_scope = 0;
@@ -1417,7 +1829,38 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
     const int64_t grid = std::min<int64_t>(ctx->n_tiles, int64_t(occ) * ctx->sms);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     WG_CUDA(cudaSetDevice(c.device));
-    if (c.dtype == WG_F32) {
+    // multi-GPU: the TMA-puller kernel when its shared-memory rings fit
+    int n_leaves_total = 0, n_rows = 0;
+    for (int k = 0; k < p.n_plans; ++k) {
+        n_leaves_total += p.plans[k].n_leaves;
+        for (int li = 0; li < p.plans[k].n_leaves; ++li)
+            n_rows += WG_NVL_TMA_LOCAL || p.plans[k].leaves[li] / ctx->R != c.gpu_index;
+    }
+    const size_t row = size_t(kThreads) * 16;
+    const size_t nvl_fixed = size_t(kNvlDepth * 3) * row;
+    const int nvl_stages =
+        n_rows == 0 ? kNvlMaxStages
+                    : int(std::min<size_t>(kNvlMaxStages, (size_t(kNvlMaxDyn) - nvl_fixed) / (size_t(n_rows) * row)));
+    if (p.need_fence && ctx->use_nvl && nvl_stages >= 2 && n_leaves_total * kWarps <= kMaxPoll &&
+        n_leaves_total <= kMaxPlans * kMaxLeaves) {
+        p.nvl_stages = nvl_stages;
+        const size_t nvl_smem = nvl_fixed + size_t(nvl_stages) * n_rows * row;
+        const int di = c.dtype == WG_F32 ? 0 : 1;
+        if (ctx->occ_nvl[di] <= 0) {
+            int o = 0;
+            cudaError_t e2 = c.dtype == WG_F32
+                                 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wagma_nvl_kernel<float>,
+                                                                                 kNvlThreads, kNvlMaxDyn)
+                                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wagma_nvl_kernel<double>,
+                                                                                 kNvlThreads, kNvlMaxDyn);
+            ctx->occ_nvl[di] = (e2 == cudaSuccess && o > 0) ? o : 1;
+        }
+        const int64_t g = std::min<int64_t>(ctx->n_tiles, int64_t(ctx->occ_nvl[di]) * ctx->sms);
+        if (c.dtype == WG_F32)
+            wagma_nvl_kernel<float><<<unsigned(g), kNvlThreads, nvl_smem, s>>>(p);
+        else
+            wagma_nvl_kernel<double><<<unsigned(g), kNvlThreads, nvl_smem, s>>>(p);
+    } else if (c.dtype == WG_F32) {
         if (p.need_fence)
             wagma_step_kernel<float, true><<<unsigned(grid), kThreads, smem, s>>>(p);
         else

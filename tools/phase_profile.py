@@ -24,6 +24,7 @@ ap.add_argument("--S", type=int, default=8)
 ap.add_argument("--nelem", type=int, default=25_559_081)
 ap.add_argument("--tau", type=int, default=10)
 ap.add_argument("--iters", type=int, default=30)
+ap.add_argument("--S2", type=int, default=0)
 a = ap.parse_args()
 rank, G, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
@@ -37,19 +38,26 @@ prof = torch.zeros(ctx.grid * 8, dtype=torch.int64, device=dev)
 ctx.lib.wg_ctx_set_profile(ctx._h, ctypes.c_void_p(prof.data_ptr()))
 ghz = 1.965
 for t in range(a.iters):
-    prof.zero_()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    opt.step(t, g)
+    for u in range(8):  # back to back (steady state), profile the last launch
+        if u == 7:
+            prof.zero_()
+            ev0.record()
+        opt.step(t * 8 + u, g)
     ev1.record()
     torch.cuda.synchronize()
-    if t >= a.iters - a.tau:
+    t = t * 8 + 7
+    if True:
         p = prof.view(-1, 8).cpu().numpy().astype(np.float64)
-        names = ["produce", "publish", "resolve", "poll", "consume", "tiles", "fence"]
-        us = {nm: p[:, i].mean() / ghz / 1000 for i, nm in enumerate(names) if nm != "tiles"}
+        if os.environ.get("WG_NVL", "1") != "0":
+            names = ["producer_total", "pull_empty_wait", "pull_poll", "pull_issue", "cons_full_wait", "x", "cons_total", "cons_ready_wait"]
+        else:
+            names = ["produce", "publish", "resolve", "poll", "consume", "tiles", "fence"]
+        us = {nm: p[:, i].mean() / ghz / 1000 for i, nm in enumerate(names) if nm not in ("tiles", "x")}
         sync = (t + 1) % a.tau == 0
-        print(f"rank{rank} t={t} {'sync ' if sync else 'group'} kernel={ev0.elapsed_time(ev1)*1000:.0f}us tiles/CTA={p[:,5].mean():.1f} "
-              + " ".join(f"{k}={v:.0f}" for k, v in us.items()), flush=True)
+        mx = {nm: p[:, i].max() / ghz / 1000 for i, nm in enumerate(names) if nm not in ("tiles", "x")}
+        print(f"rank{rank} t={t} {'sync ' if sync else 'group'} kernel={ev0.elapsed_time(ev1)*1000:.0f}us "
+              + " ".join(f"{k}={v:.0f}/{mx[k]:.0f}" for k, v in us.items()), flush=True)
 ctx.lib.wg_ctx_set_profile(ctx._h, None)
 ctx.check()
 dist.barrier()
