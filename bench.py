@@ -56,6 +56,12 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--grace-us", type=float, default=100.0)
+    # imbalance experiments (not part of the default metric line)
+    ap.add_argument("--blocking", action="store_true", help="blocking group allreduce (beta) instead of alpha")
+    ap.add_argument("--base-ms", type=float, default=0.0, help="device-side 'compute' delay per step, every GPU")
+    ap.add_argument("--victims", type=int, default=0, help="StragglerPolicy victims per iteration")
+    ap.add_argument("--extra-ms", type=float, default=0.0, help="extra delay of a victim rank's GPU")
+    ap.add_argument("--straggler-seed", type=int, default=12)
     return ap.parse_args()
 
 
@@ -268,9 +274,19 @@ def run_ours(a):
         return max_over_ranks(x, device=dev)
 
     ctx = DeviceContext(a.P, a.S, a.n, dtype=dt, tau=a.tau, n_gpus=G, gpu_index=rank, device=dev.index,
-                        grace_us=a.grace_us, timeout_s=30.0)
-    cfg = OptimizerConfig(T=1 << 30, S=a.S, tau=a.tau, alpha=True, eta=EtaSchedule(value=0.1),
-                          update_rule="momentum", momentum=0.9)
+                        grace_us=a.grace_us, timeout_s=30.0, activation_enabled=not a.blocking)
+    cfg = OptimizerConfig(T=1 << 30, S=a.S, tau=a.tau, alpha=not a.blocking, beta=a.blocking,
+                          eta=EtaSchedule(value=0.1), update_rule="momentum", momentum=0.9)
+    from paper_2005_00124_b200.straggler import StragglerPolicy
+    policy = StragglerPolicy(a.victims, a.extra_ms, selection_seed=a.straggler_seed) if a.victims else None
+
+    def delay(t):
+        """compute_delay (netsim.py:103-117) as a device spin before this GPU's step."""
+        ms = a.base_ms
+        if policy is not None and set(local) & policy.victims(t, a.P):
+            ms += a.extra_ms
+        if ms > 0:
+            ctx.delay(int(ms * 1e6))
     gen = torch.Generator(device=dev).manual_seed(1234)
     w0 = torch.randn(a.n, generator=gen, device=dev, dtype=dt) * 0.02
     opt = GroupAveragingOptimizer(ctx, cfg, w0)
@@ -282,6 +298,7 @@ def run_ours(a):
 
     t = 0
     for _ in range(a.warmup):
+        delay(t)
         opt.step(t, {r: gpool[r][t % 2] for r in local})
         t += 1
     sampler = ClockSampler(dev.index) if rank == 0 else None
@@ -296,6 +313,7 @@ def run_ours(a):
     t_first = t
     start.record(stream)
     for k in range(a.steps):
+        delay(t)
         ev[k][0].record(stream)
         opt.step(t, {r: gpool[r][t % 2] for r in local})
         ev[k][1].record(stream)
@@ -380,6 +398,21 @@ def run_ours(a):
                 "vs_baseline": None, "dtype": a.dtype, "data": "synthetic", "config": config_dict(a, G),
                 "group_avg_gbs": group_avg_gbs, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": gpu_launches, "clocks": clocks}
+        if a.blocking or a.victims or a.base_ms:
+            from paper_2005_00124_b200.optim import is_sync_iteration
+            stale = total = 0
+            for v in range(max(0, t - ctx.ring_depth + 1), t):
+                if is_sync_iteration(v, a.tau) or a.blocking:
+                    continue
+                stamps, locked = ctx.query_version(v)
+                if locked:
+                    total += len(stamps)
+                    stale += sum(1 for st in stamps if st != v)
+            line["imbalance"] = {"activation": "blocking (beta)" if a.blocking else "wait-avoiding (alpha)",
+                                 "base_ms": a.base_ms, "victims_per_iteration": a.victims, "extra_ms": a.extra_ms,
+                                 "selection_seed": a.straggler_seed,
+                                 "stale_contribution_fraction": (stale / total) if total else None}
+            line["config"]["activation"] = line["imbalance"]["activation"]
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
