@@ -80,7 +80,7 @@ if rank == 0:
                       "S": S, "batch_per_gpu": a.batch, "images": "synthetic 224x224", "amp": "bf16",
                       "train_iters_per_s": 1000.0 * a.steps / total_ms,
                       "wagma_step_ms": step_ms / a.steps, "wagma_share": step_ms / total_ms,
-                      "final_loss": float(loss)}))
+                      "final_loss": float(loss.detach())}))
 ctx.close()
 if world > 1:
     dist.destroy_process_group()
