@@ -84,11 +84,14 @@ struct Layout {
     int64_t desc;      // Desc [Dv]  (used on GPU 0 only)
     int64_t flags;     // int64 [R][n_tiles][warps]: latest stamp published per warp-tile
     int64_t ring;      // T [R][D][npad]: send ring
+    int64_t red_flags; // int64 [R][n_tiles]: latest version whose reduced tile is published (multi-GPU)
+    int64_t red_ring;  // T [R][D][npad]: reduced tiles owned by the rank (split sums)
     int64_t total;
 };
 
 constexpr int kAnnounceStride = 16;  // int64 words (128 B)
 constexpr int kWarps = kThreads / 32;
+constexpr int kSplitMaxP = 8;  // split sums (reduce-scatter + all-gather) up to this many ranks
 constexpr int64_t kNever = INT64_MIN / 2;
 
 enum VersionMode : int32_t { kLive = 0, kForced = 1, kBlocking = 2, kSync = 3 };
@@ -112,7 +115,9 @@ struct DevVersion {
 
 struct DevPlan {
     int32_t vidx, n_leaves, log_leaves, divisor, n_members, divisor_pow2;
+    int32_t n_owners, pad;          // distinct group members (split-sum owners)
     int16_t leaves[kMaxLeaves];
+    int16_t owners[kMaxLeaves];     // sorted distinct members (split-sum owners, see split_owner)
     int8_t members[kMaxJobs];
 };
 
@@ -131,6 +136,8 @@ struct LaunchParams {
     long long* prof;  // optional per-CTA phase cycle counters [grid][8]
     int32_t fence_scope;  // 0 sys, 1 gpu (default), 2 none (timing experiments only)
     int32_t nvl_stages;   // leaf-ring stages of the multi-GPU TMA kernel
+    int32_t split_stages; // reduced-tile ring stages of the split kernel
+    int32_t pad3;
 };
 
 // ---------------------------------------------------------------------------
@@ -273,6 +280,14 @@ __device__ __forceinline__ int64_t* flag_ptr(const LaunchParams& p, int rank, in
 template <typename T>
 __device__ __forceinline__ T* ring_ptr(const LaunchParams& p, int rank, int slot) {
     return reinterpret_cast<T*>(rank_base(p, rank) + p.L.ring) + (int64_t(rank % p.R) * p.D + slot) * p.npad;
+}
+__device__ __forceinline__ int64_t* red_flag_ptr(const LaunchParams& p, int rank, int64_t tile) {
+    return reinterpret_cast<int64_t*>(rank_base(p, rank) + p.L.red_flags) + int64_t(rank % p.R) * p.n_tiles + tile;
+}
+template <typename T>
+__device__ __forceinline__ T* red_ptr(const LaunchParams& p, int rank, int64_t version) {
+    return reinterpret_cast<T*>(rank_base(p, rank) + p.L.red_ring) +
+           (int64_t(rank % p.R) * p.D + version % p.D) * p.npad;
 }
 __device__ __forceinline__ Desc* desc_ptr(const LaunchParams& p, int64_t version) {
     return reinterpret_cast<Desc*>(p.base[0] + p.L.desc) + (version % p.Dv);
@@ -418,6 +433,7 @@ struct SmemCtl {
     int8_t leaf_src[kMaxPlans][kMaxLeaves];  // >=0: stage of job; -1 poll; -2 ready
     int16_t leaf_slot[kMaxPlans][kMaxLeaves];
     int32_t plan_polls[kMaxPlans];
+    int32_t plan_split[kMaxPlans];
     int32_t activator[kMaxVersions];
     int32_t abort;
 };
@@ -987,6 +1003,7 @@ constexpr int kPollPerLane = 8;
 constexpr int kPullBatch = 8;  // tiles whose flags are polled and copies issued together
 constexpr int kPubChunk = 8;   // tiles published together (one fence per chunk)
 constexpr int kPubRing = 16;   // per-chunk producer-completion counters (drift bound kPubRing/2 chunks)
+constexpr int kRedRing = 32;   // per-tile reducer counters (reducers drift < kNvlMaxStages tiles)
 constexpr int kMaxPoll = 32 * kPollPerLane;  // (leaf, warp) flags polled per tile
 
 __device__ __forceinline__ unsigned smem_u32(const void* ptr) {
@@ -1032,6 +1049,90 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                      smem_u32(dst)),
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
+}
+
+// Producer warps of the multi-GPU kernels (warps 0..7): local step of every
+// job for every tile of this CTA, send-ring install, and the tiles'
+// readiness flags published in chunks of kPubChunk by the last warp to
+// finish a chunk (one GPU-scope fence, cumulative over the other warps'
+// stores acquired through the shared-memory counter). Never waits on a peer.
+template <typename T>
+__device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename Tr<T>::V* ring, int64_t my_ntiles,
+                                                unsigned* pub_count) {
+    using V = typename Tr<T>::V;
+    const int lane = threadIdx.x & 31;
+    const int J = p.n_jobs;
+    unsigned my_tiles = 0;
+    const int64_t n_items = my_ntiles * J;
+#pragma unroll
+    for (int d = 0; d < kNvlDepth; ++d) {
+        if (d < n_items)
+            issue_item<T>(p, int64_t(blockIdx.x) + (d / J) * int64_t(gridDim.x), d % J, ring + d * 3 * kThreads);
+        cp_async_commit();
+    }
+    int64_t i = 0;
+    for (int64_t kk = 0; kk < my_ntiles; ++kk) {
+        const int64_t tile = int64_t(blockIdx.x) + kk * gridDim.x;
+        for (int j = 0; j < J; ++j, ++i) {
+            cp_async_wait<kNvlDepth - 1>();
+            V* slot = ring + (i % kNvlDepth) * 3 * kThreads;
+            compute_item<T, false>(p, tile, j, slot, nullptr);
+            const int64_t nx = i + kNvlDepth;
+            if (nx < n_items)
+                issue_item<T>(p, int64_t(blockIdx.x) + (nx / J) * int64_t(gridDim.x), int(nx % J), slot);
+            cp_async_commit();
+        }
+        // Tiles are published in chunks of kPubChunk: the last producer
+        // warp to finish a chunk issues one GPU-scope fence (cumulative
+        // over the other warps' stores, acquired through the shared-memory
+        // counter) and writes the chunk's per-warp flags with all lanes.
+        // No other warp ever waits on a fence.
+        const bool chunk_end = ((kk + 1) % kPubChunk == 0) || (kk + 1 == my_ntiles);
+        if (chunk_end) {
+            __syncwarp();
+            unsigned old = 0;
+            if (lane == 0) {
+                unsigned* cnt = &pub_count[(kk / kPubChunk) & (kPubRing - 1)];
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                             : "=r"(old)
+                             : "r"(smem_u32(cnt))
+                             : "memory");
+                if (old == kWarps - 1) *cnt = 0;
+            }
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old == kWarps - 1) {
+                if (p.fence_scope == 0)
+                    fence_sys();
+                else if (p.fence_scope == 1)
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                const int64_t k0 = kk - (kk % kPubChunk);
+                const int nk = int(kk - k0 + 1);
+                for (int e = lane; e < nk * J * kWarps; e += 32) {
+                    const int w = e % kWarps, j = (e / kWarps) % J, b = e / (kWarps * J);
+                    const DevJob& jb = p.jobs[j];
+                    if (jb.produces)
+                        st_relaxed_sys(flag_ptr(p, jb.rank, int64_t(blockIdx.x) + (k0 + b) * gridDim.x, w),
+                                       jb.version);
+                }
+            }
+        }
+        ++my_tiles;
+        // bound the drift between producer warps (the counter ring)
+        if ((kk + 1) % (kPubChunk * kPubRing / 2) == 0) {
+            // named barrier over the 8 producer warps, OR-reducing the abort
+            // flag so that all of them leave together
+            int stop;
+            asm volatile(
+                "{\n .reg .pred a, b;\n setp.ne.s32 a, %1, 0;\n bar.red.or.pred b, 1, %2, a;\n"
+                " selp.s32 %0, 1, 0, b;\n}\n"
+                : "=r"(stop)
+                : "r"(int(aborted(p))), "n"(kThreads)
+                : "memory");
+            if (stop) break;
+        }
+    }
+    cp_async_wait<0>();
+    return my_tiles;
 }
 
 template <typename T>
@@ -1086,76 +1187,8 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
 
     if (warp < kWarps) {
         // ---------------- producers ----------------
-        const int64_t n_items = my_ntiles * J;
-#pragma unroll
-        for (int d = 0; d < kNvlDepth; ++d) {
-            if (d < n_items)
-                issue_item<T>(p, int64_t(blockIdx.x) + (d / J) * int64_t(gridDim.x), d % J, ring + d * 3 * kThreads);
-            cp_async_commit();
-        }
-        int64_t i = 0;
         const long long pc0 = clock64();
-        for (int64_t kk = 0; kk < my_ntiles; ++kk) {
-            const int64_t tile = int64_t(blockIdx.x) + kk * gridDim.x;
-            for (int j = 0; j < J; ++j, ++i) {
-                cp_async_wait<kNvlDepth - 1>();
-                V* slot = ring + (i % kNvlDepth) * 3 * kThreads;
-                compute_item<T, false>(p, tile, j, slot, nullptr);
-                const int64_t nx = i + kNvlDepth;
-                if (nx < n_items)
-                    issue_item<T>(p, int64_t(blockIdx.x) + (nx / J) * int64_t(gridDim.x), int(nx % J), slot);
-                cp_async_commit();
-            }
-            // Tiles are published in chunks of kPubChunk: the last producer
-            // warp to finish a chunk issues one GPU-scope fence (cumulative
-            // over the other warps' stores, acquired through the shared-memory
-            // counter) and writes the chunk's per-warp flags with all lanes.
-            // No other warp ever waits on a fence.
-            const bool chunk_end = ((kk + 1) % kPubChunk == 0) || (kk + 1 == my_ntiles);
-            if (chunk_end) {
-                __syncwarp();
-                unsigned old = 0;
-                if (lane == 0) {
-                    unsigned* cnt = &pub_count[(kk / kPubChunk) & (kPubRing - 1)];
-                    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
-                                 : "=r"(old)
-                                 : "r"(smem_u32(cnt))
-                                 : "memory");
-                    if (old == kWarps - 1) *cnt = 0;
-                }
-                old = __shfl_sync(0xffffffffu, old, 0);
-                if (old == kWarps - 1) {
-                    if (p.fence_scope == 0)
-                        fence_sys();
-                    else if (p.fence_scope == 1)
-                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    const int64_t k0 = kk - (kk % kPubChunk);
-                    const int nk = int(kk - k0 + 1);
-                    for (int e = lane; e < nk * J * kWarps; e += 32) {
-                        const int w = e % kWarps, j = (e / kWarps) % J, b = e / (kWarps * J);
-                        const DevJob& jb = p.jobs[j];
-                        if (jb.produces)
-                            st_relaxed_sys(flag_ptr(p, jb.rank, int64_t(blockIdx.x) + (k0 + b) * gridDim.x, w),
-                                           jb.version);
-                    }
-                }
-            }
-            ++my_tiles;
-            // bound the drift between producer warps (the counter ring)
-            if ((kk + 1) % (kPubChunk * kPubRing / 2) == 0) {
-                // named barrier over the 8 producer warps, OR-reducing the abort
-                // flag so that all of them leave together
-                int stop;
-                asm volatile(
-                    "{\n .reg .pred a, b;\n setp.ne.s32 a, %1, 0;\n bar.red.or.pred b, 1, %2, a;\n"
-                    " selp.s32 %0, 1, 0, b;\n}\n"
-                    : "=r"(stop)
-                    : "r"(int(aborted(p))), "n"(kThreads)
-                    : "memory");
-                if (stop) break;
-            }
-        }
-        cp_async_wait<0>();
+        my_tiles = nvl_produce<T>(p, ring, my_ntiles, pub_count);
         if (p.prof && tid == 0) p.prof[blockIdx.x * 8 + 0] = clock64() - pc0;
     } else if (warp == 2 * kWarps) {
         // ---------------- puller ----------------
@@ -1347,6 +1380,497 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     }
 }
 
+// ---------------------------------------------------------------------------
+// multi-GPU kernel with split sums (reduce-scatter + all-gather)
+//
+// A group whose members all contributed fresh W' (every stamp == version)
+// and that spans GPUs is summed split: tile t is reduced only by
+// split_owner(t) (same butterfly order, so the bits are unchanged),
+// which publishes the reduced tile; every other member copies that one tile
+// instead of all S leaves. NVLink ingress per GPU drops from (S-1)·N to
+// about 2(S-1)/S·N. Groups with a stale member are summed by the pull.
+//
+// Warps: 0-7 producers (as in wagma_nvl_kernel); stream A (tiles this GPU
+// reduces itself, and every tile of pulled groups): warp 8 puller, warps
+// 9-16 reducers (sum, publish owned reduced tiles, write W_{t+1}); stream B
+// (tiles reduced by an owner on another GPU): warp 17 puller (waits for the
+// owner's reduced-tile flag, one TMA copy per tile), warps 18-21 finishers.
+// Stream A never waits on stream B, so no cross-GPU wait cycle exists.
+// ---------------------------------------------------------------------------
+
+constexpr int kSplitThreads = 22 * 32;
+constexpr int kFinThreads = 4 * 32;
+
+// Owner of a tile of a split sum: rotates along each CTA's tile sequence so
+// every CTA reduces 1/n_owners of its tiles (tile t is the (t / grid)-th tile
+// of CTA t % grid; the grid is identical on every GPU).
+__device__ __forceinline__ int split_owner(const DevPlan& P_, int64_t tile) {
+    return P_.owners[(tile / gridDim.x) % P_.n_owners];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __grid_constant__ LaunchParams p) {
+    using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
+    extern __shared__ __align__(128) unsigned char dyn_smem[];
+    __shared__ SmemCtl sm;
+    __shared__ __align__(8) uint64_t fullA[kNvlMaxStages], emptyA[kNvlMaxStages];
+    __shared__ __align__(8) uint64_t fullB[kNvlMaxStages], emptyB[kNvlMaxStages];
+    __shared__ int64_t metaA_tile[kNvlMaxStages], metaB_tile[kNvlMaxStages];
+    __shared__ unsigned metaA_mask[kNvlMaxStages], metaB_mask[kNvlMaxStages];
+    __shared__ int leaf_base[kMaxPlans + 1];
+    __shared__ volatile int ready;
+    __shared__ int16_t poll_q[kMaxPoll];
+    __shared__ int8_t poll_w[kMaxPoll];
+    __shared__ int64_t poll_s[kMaxPoll];
+    __shared__ int plan_poll_base[kMaxPlans], plan_poll_cnt[kMaxPlans];
+    __shared__ unsigned pub_count[kPubRing];
+    __shared__ unsigned red_count[kRedRing];
+    __shared__ int64_t bt_tile[kPullBatch];
+    __shared__ unsigned bt_mask[kPullBatch];
+    __shared__ int bt_n;
+    __shared__ int cell_pref[kPullBatch * kMaxPlans + 1];
+    __shared__ int64_t btB_tile[kPullBatch];
+    __shared__ unsigned btB_mask[kPullBatch];
+    __shared__ int btB_n;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int NSA = p.nvl_stages, NSB = p.split_stages, NP = p.n_plans;
+    if (tid == 0) {
+        sm.abort = 0;
+        ready = 0;
+        for (int st = 0; st < NSA; ++st) {
+            mbar_init(&fullA[st], 1);
+            mbar_init(&emptyA[st], kWarps);
+        }
+        for (int st = 0; st < NSB; ++st) {
+            mbar_init(&fullB[st], 1);
+            mbar_init(&emptyB[st], kFinThreads / 32);
+        }
+        int acc = 0;
+        for (int pl = 0; pl < NP; ++pl) {
+            leaf_base[pl] = acc;
+            acc += p.plans[pl].n_leaves;
+        }
+        leaf_base[NP] = acc;
+    }
+    if (tid < kMaxVersions) sm.activator[tid] = 0;
+    if (tid < kPubRing) pub_count[tid] = 0;
+    if (tid < kRedRing) red_count[tid] = 0;
+    __syncthreads();
+    const int NL = leaf_base[NP];
+    V* ringA = reinterpret_cast<V*>(dyn_smem);              // [NSA][NL][kThreads]
+    V* ringB = ringA + size_t(NSA) * NL * kThreads;           // [NSB][NP][kThreads]
+    V* ring = ringB + size_t(NSB) * NP * kThreads;            // [kNvlDepth][3][kThreads]
+    const int64_t my_ntiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const unsigned tile_bytes = unsigned(p.tile_elems * int64_t(sizeof(T)));
+    unsigned my_tiles = 0;
+    // plans of a tile handled by stream A (mask A) or stream B (mask B)
+    auto masks = [&](int64_t tile, unsigned& ma, unsigned& mb) {
+        ma = mb = 0;
+        for (int pl = 0; pl < NP; ++pl) {
+            const DevPlan& P_ = p.plans[pl];
+            const bool remote_owner = sm.plan_split[pl] && split_owner(P_, tile) / p.R != p.gpu_index;
+            (remote_owner ? mb : ma) |= 1u << pl;
+        }
+    };
+    auto acquire_for_tma = [&]() {
+        if (p.fence_scope == 0)
+            fence_sys();
+        else
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    };
+
+    const long long t_start = clock64();
+    auto prof_set = [&](int slot, long long v) {
+        if (p.prof) p.prof[blockIdx.x * 8 + slot] = v;
+    };
+    if (warp < kWarps) {
+        my_tiles = nvl_produce<T>(p, ring, my_ntiles, pub_count);
+        if (tid == 0) prof_set(0, clock64() - t_start);
+    } else if (warp == kWarps) {
+        // ---------------- stream A puller ----------------
+        if (blockIdx.x == 0) control_phase(p, sm.activator);
+        bool resolved = resolve_core<T>(p, sm, lane, 32, [] { __syncwarp(); });
+        __syncwarp();
+        if (resolved && lane == 0) {
+            int n_poll = 0;
+            for (int pl = 0; pl < NP; ++pl) {
+                const DevPlan& P_ = p.plans[pl];
+                const int64_t v = p.versions[P_.vidx].version;
+                plan_poll_base[pl] = n_poll;
+                // split when every member is timely and the group spans >= 4
+                // GPUs (fewer: the reduced-tile copies save little NVLink)
+                bool split = P_.n_owners == P_.n_leaves && P_.n_owners >= 2;
+                bool remote = false;
+                unsigned gpus = 0;
+                for (int li = 0; li < P_.n_leaves; ++li) {
+                    const int q = P_.leaves[li];
+                    split = split && sm.stamps[P_.vidx][q] == v;
+                    remote = remote || q / p.R != p.gpu_index;
+                    gpus |= 1u << (q / p.R);
+                }
+                split = split && __popc(gpus) >= 4;
+                for (int li = 0; li < P_.n_leaves; ++li) {
+                    const int q = P_.leaves[li];
+                    if (sm.leaf_src[pl][li] == kSrcReady) continue;
+                    if (sm.leaf_src[pl][li] >= 0) sm.leaf_slot[pl][li] = int16_t(slot_of(p, sm.stamps[P_.vidx][q]));
+                    for (int w = 0; w < kWarps; ++w) {
+                        if (n_poll == kMaxPoll) {
+                            raise_error(p, WG_EINVAL, n_poll);
+                            break;
+                        }
+                        poll_q[n_poll] = int16_t(q);
+                        poll_w[n_poll] = int8_t(w);
+                        poll_s[n_poll] = sm.stamps[P_.vidx][q];
+                        ++n_poll;
+                    }
+                }
+                plan_poll_cnt[pl] = n_poll - plan_poll_base[pl];
+                sm.plan_split[pl] = split && remote;
+            }
+            __threadfence_block();
+            ready = aborted(p) ? 2 : 1;
+        } else if (!resolved && lane == 0) {
+            ready = 2;
+        }
+        __syncwarp();
+        resolved = resolved && ready == 1;
+        const int batch = NSA - 1 < kPullBatch ? (NSA > 1 ? NSA - 1 : 1) : kPullBatch;
+        int64_t kA = 0, kc = 0;
+        bool ok = resolved;
+        while (ok) {
+            // next batch of tiles with stream-A work
+            if (lane == 0) {
+                int n = 0;
+                while (kc < my_ntiles && n < batch) {
+                    const int64_t tile = int64_t(blockIdx.x) + kc * gridDim.x;
+                    unsigned ma, mb;
+                    masks(tile, ma, mb);
+                    ++kc;
+                    if (!ma) continue;
+                    bt_tile[n] = tile;
+                    bt_mask[n] = ma;
+                    ++n;
+                }
+                bt_n = n;
+            }
+            __syncwarp();
+            kc = __shfl_sync(0xffffffffu, kc, 0);
+            const int nb = bt_n;
+            if (nb == 0) break;
+            for (int b = 0; b < nb && ok; ++b) {
+                const int64_t k = kA + b;
+                if (k >= NSA && !mbar_wait(p, &emptyA[k % NSA], unsigned((k / NSA - 1) & 1))) ok = false;
+            }
+            if (!ok) {
+                if (lane == 0) raise_error(p, WG_ETIMEOUT, kA);
+                break;
+            }
+            // producer flags of every leaf of the batch's active plans, all
+            // loads in flight together (producers never wait, so waiting for
+            // the whole batch cannot deadlock)
+            if (lane == 0) {
+                int acc = 0;
+                for (int c = 0; c < nb * NP; ++c) {
+                    cell_pref[c] = acc;
+                    if (bt_mask[c / NP] >> (c % NP) & 1) acc += plan_poll_cnt[c % NP];
+                }
+                cell_pref[nb * NP] = acc;
+            }
+            __syncwarp();
+            const int total = cell_pref[nb * NP];
+            int rc = 0;
+            for (int base = 0; base < total && !rc; base += 32 * kPollPerLane) {
+                const int64_t* fp[kPollPerLane];
+                int64_t want[kPollPerLane], v[kPollPerLane];
+#pragma unroll
+                for (int r = 0; r < kPollPerLane; ++r) {
+                    const int e = base + lane + 32 * r;
+                    fp[r] = nullptr;
+                    if (e >= total) continue;
+                    int c = 0;
+                    while (cell_pref[c + 1] <= e) ++c;
+                    const int idx = plan_poll_base[c % NP] + (e - cell_pref[c]);
+                    fp[r] = flag_ptr(p, poll_q[idx], bt_tile[c / NP], poll_w[idx]);
+                    want[r] = poll_s[idx];
+                    v[r] = ld_relaxed_sys(fp[r]);
+                }
+#pragma unroll
+                for (int r = 0; r < kPollPerLane; ++r) {
+                    if (!fp[r] || rc) continue;
+                    const uint64_t t0 = globaltimer();
+                    int it = 0;
+                    while (v[r] < want[r]) {
+                        if ((++it & 63) == 0 && (globaltimer() - t0 > uint64_t(p.timeout_ns) || aborted(p))) {
+                            rc = WG_ETIMEOUT;
+                            break;
+                        }
+                        __nanosleep(32);
+                        v[r] = ld_relaxed_sys(fp[r]);
+                    }
+                    if (!rc && v[r] >= want[r] + p.D) rc = WG_EPROTO;
+                    if (rc) raise_error(p, rc, want[r]);
+                }
+            }
+            if (__any_sync(0xffffffffu, rc != 0)) break;
+            acquire_for_tma();
+            if (lane == 0) {
+                for (int b = 0; b < nb; ++b) {
+                    const int st = int((kA + b) % NSA);
+                    unsigned rows = 0;
+                    for (int pl = 0; pl < NP; ++pl)
+                        if (bt_mask[b] >> pl & 1) rows += p.plans[pl].n_leaves;
+                    metaA_tile[st] = bt_tile[b];
+                    metaA_mask[st] = bt_mask[b];
+                    mbar_arrive_expect_tx(&fullA[st], rows * tile_bytes);
+                }
+            }
+            __syncwarp();
+            for (int e = lane; e < nb * NL; e += 32) {
+                const int b = e / NL, f = e % NL;
+                int pl = 0;
+                while (leaf_base[pl + 1] <= f) ++pl;
+                if (!(bt_mask[b] >> pl & 1)) continue;
+                const int li = f - leaf_base[pl];
+                const int st = int((kA + b) % NSA);
+                const T* src =
+                    ring_ptr<T>(p, p.plans[pl].leaves[li], sm.leaf_slot[pl][li]) + bt_tile[b] * p.tile_elems;
+                bulk_g2s(ringA + (size_t(st) * NL + f) * kThreads, src, tile_bytes, &fullA[st]);
+            }
+            __syncwarp();
+            kA += nb;
+        }
+        // end of stream A
+        if (kA >= NSA && !mbar_wait(p, &emptyA[kA % NSA], unsigned((kA / NSA - 1) & 1))) ok = false;
+        if (lane == 0) {
+            metaA_tile[kA % NSA] = -1;
+            mbar_arrive(&fullA[kA % NSA]);
+            prof_set(1, clock64() - t_start);
+        }
+    } else if (warp <= 2 * kWarps) {
+        // ---------------- stream A reducers ----------------
+        const int ctid = tid - (kWarps + 1) * 32;
+        while (ready == 0) __nanosleep(64);
+        long long wait_a = 0;
+        for (int64_t kA = 0; ready == 1; ++kA) {
+            const int st = int(kA % NSA);
+            const long long w0 = clock64();
+            if (!mbar_wait(p, &fullA[st], unsigned((kA / NSA) & 1))) {
+                if (lane == 0) raise_error(p, WG_ETIMEOUT, kA);
+                break;
+            }
+            wait_a += clock64() - w0;
+            const int64_t tile = metaA_tile[st];
+            if (tile < 0) break;
+            const unsigned mask = metaA_mask[st];
+            const int64_t idx = tile * p.tile_elems + int64_t(ctid) * E;
+            const V* lb = ringA + size_t(st) * NL * kThreads;
+            bool owned = false;
+            for (int pl = 0; pl < NP; ++pl) {
+                if (!(mask >> pl & 1)) continue;
+                const DevPlan& P_ = p.plans[pl];
+                const int base = leaf_base[pl];
+                auto fetch = [&](int leaf) -> V { return lb[(base + leaf) * kThreads + ctid]; };
+                const V acc = tree_sum<T>(fetch, P_.log_leaves);
+                if (sm.plan_split[pl]) {  // this GPU owns the tile: publish the reduced tile
+                    __stcg(reinterpret_cast<V*>(red_ptr<T>(p, split_owner(P_, tile),
+                                                          p.versions[P_.vidx].version) + idx), acc);
+                    owned = true;
+                }
+                auto own_wp = [&](int j) -> V {
+                    const DevJob& jb = p.jobs[j];
+                    return __ldcg(reinterpret_cast<const V*>(ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + idx));
+                };
+                finish_members<T>(p, sm, P_, acc, idx, own_wp);
+            }
+            if (owned) {
+                // the last reducer warp of the tile: one fence, then the flags
+                __syncwarp();
+                unsigned old = 0;
+                if (lane == 0) {
+                    unsigned* cnt = &red_count[kA & (kRedRing - 1)];
+                    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                                 : "=r"(old)
+                                 : "r"(smem_u32(cnt))
+                                 : "memory");
+                    if (old == kWarps - 1) *cnt = 0;
+                }
+                old = __shfl_sync(0xffffffffu, old, 0);
+                if (old == kWarps - 1) {
+                    if (p.fence_scope == 0)
+                        fence_sys();
+                    else
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    if (lane < NP && (mask >> lane & 1) && sm.plan_split[lane]) {
+                        const DevPlan& P_ = p.plans[lane];
+                        st_relaxed_sys(red_flag_ptr(p, split_owner(P_, tile), tile),
+                                       p.versions[P_.vidx].version);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&emptyA[st]);
+        }
+        if (ctid == 0) {
+            prof_set(3, wait_a);
+            prof_set(4, clock64() - t_start);
+        }
+    } else if (warp == 2 * kWarps + 1) {
+        // ---------------- stream B puller ----------------
+        // Batches of up to kPullBatch tiles reduced on other GPUs: all the
+        // owners' reduced-tile flags loaded at once, then tile by tile (in
+        // order) wait, copy the reduced tiles.
+        while (ready == 0) __nanosleep(64);
+        int64_t kB = 0, kc = 0;
+        bool ok = ready == 1;
+        int batch = NSB - 1 < kPullBatch ? (NSB > 1 ? NSB - 1 : 1) : kPullBatch;
+        batch = batch * NP > 32 ? (32 / NP > 0 ? 32 / NP : 1) : batch;  // one flag per lane
+        while (ok) {
+            if (lane == 0) {
+                int n = 0;
+                while (kc < my_ntiles && n < batch) {
+                    const int64_t tile = int64_t(blockIdx.x) + kc * gridDim.x;
+                    unsigned ma, mb;
+                    masks(tile, ma, mb);
+                    ++kc;
+                    if (!mb) continue;
+                    btB_tile[n] = tile;
+                    btB_mask[n] = mb;
+                    ++n;
+                }
+                btB_n = n;
+            }
+            __syncwarp();
+            kc = __shfl_sync(0xffffffffu, kc, 0);
+            const int nb = btB_n;
+            if (nb == 0) break;
+            // lane e -> (tile b = e / NP, plan e % NP)
+            int64_t x = 0, want = 0;
+            const int64_t* fp = nullptr;
+            const int e = lane;
+            if (e < nb * NP && (btB_mask[e / NP] >> (e % NP) & 1)) {
+                const DevPlan& P_ = p.plans[e % NP];
+                want = p.versions[P_.vidx].version;
+                fp = red_flag_ptr(p, split_owner(P_, btB_tile[e / NP]), btB_tile[e / NP]);
+                x = ld_relaxed_sys(fp);
+            }
+            int rc = 0;
+            // usual case: every owner already published -> one fence for the batch
+            const bool all_ready = __all_sync(0xffffffffu, !fp || x >= want);
+            if (all_ready) acquire_for_tma();
+            for (int bb = 0; bb < nb && ok; ++bb) {
+                const int64_t k = kB + bb;
+                const int st = int(k % NSB);
+                if (k >= NSB && !mbar_wait(p, &emptyB[st], unsigned((k / NSB - 1) & 1))) {
+                    ok = false;
+                    break;
+                }
+                if (!all_ready && fp && e / NP == bb) {
+                    const uint64_t t0 = globaltimer();
+                    int it = 0;
+                    while (x < want) {
+                        if ((++it & 63) == 0 && (globaltimer() - t0 > uint64_t(p.timeout_ns) || aborted(p))) {
+                            rc = WG_ETIMEOUT;
+                            break;
+                        }
+                        __nanosleep(32);
+                        x = ld_relaxed_sys(fp);
+                    }
+                    if (!rc && x >= want + p.D) rc = WG_EPROTO;
+                    if (rc) raise_error(p, rc, want);
+                }
+                if (__any_sync(0xffffffffu, rc != 0)) {
+                    ok = false;
+                    break;
+                }
+                if (!all_ready) acquire_for_tma();
+                const int64_t tile = btB_tile[bb];
+                const unsigned mb = btB_mask[bb];
+                if (lane == 0) {
+                    metaB_tile[st] = tile;
+                    metaB_mask[st] = mb;
+                    mbar_arrive_expect_tx(&fullB[st], unsigned(__popc(mb)) * tile_bytes);
+                }
+                __syncwarp();
+                if (lane < NP && (mb >> lane & 1)) {
+                    const DevPlan& P_ = p.plans[lane];
+                    const T* src = red_ptr<T>(p, split_owner(P_, tile), p.versions[P_.vidx].version) +
+                                   tile * p.tile_elems;
+                    bulk_g2s(ringB + (size_t(st) * NP + lane) * kThreads, src, tile_bytes, &fullB[st]);
+                }
+                __syncwarp();
+            }
+            if (!ok) {
+                if (lane == 0) raise_error(p, WG_ETIMEOUT, kB);
+                break;
+            }
+            kB += nb;
+        }
+        if (kB >= NSB && !mbar_wait(p, &emptyB[kB % NSB], unsigned((kB / NSB - 1) & 1))) ok = false;
+        if (lane == 0) {
+            metaB_tile[kB % NSB] = -1;
+            mbar_arrive(&fullB[kB % NSB]);
+            prof_set(5, clock64() - t_start);
+        }
+    } else {
+        // ---------------- stream B finishers (2 vectors per thread) ----------------
+        const int ftid = tid - (2 * kWarps + 2) * 32;
+        while (ready == 0) __nanosleep(64);
+        long long wait_b = 0;
+        for (int64_t kB = 0; ready == 1; ++kB) {
+            const int st = int(kB % NSB);
+            const long long w0 = clock64();
+            if (!mbar_wait(p, &fullB[st], unsigned((kB / NSB) & 1))) {
+                if (lane == 0) raise_error(p, WG_ETIMEOUT, kB);
+                break;
+            }
+            wait_b += clock64() - w0;
+            const int64_t tile = metaB_tile[st];
+            if (tile < 0) break;
+            const unsigned mask = metaB_mask[st];
+            const V* lb = ringB + size_t(st) * NP * kThreads;
+            for (int h = 0; h < kThreads / kFinThreads; ++h) {
+                const int vec = ftid + h * kFinThreads;
+                const int64_t idx = tile * p.tile_elems + int64_t(vec) * E;
+                for (int pl = 0; pl < NP; ++pl) {
+                    if (!(mask >> pl & 1)) continue;
+                    auto own_wp = [&](int j) -> V {
+                        const DevJob& jb = p.jobs[j];
+                        return __ldcg(
+                            reinterpret_cast<const V*>(ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + idx));
+                    };
+                    finish_members<T>(p, sm, p.plans[pl], lb[pl * kThreads + vec], idx, own_wp);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&emptyB[st]);
+        }
+        if (ftid == 0) {
+            prof_set(6, wait_b);
+            prof_set(7, clock64() - t_start);
+        }
+    }
+    if (aborted(p)) sm.abort = 1;
+    publish_slots(p, sm.abort ? 0u : my_tiles);
+    if (blockIdx.x == 0) {
+        __syncthreads();
+        const bool res = ready == 1;
+        if (tid < p.n_jobs) {
+            const DevJob& jb = p.jobs[tid];
+            wg_job_status stt;
+            stt.version = jb.version;
+            stt.contrib_stamp = (jb.kind == WG_JOB_LOCAL_STEP || !res) ? jb.version : sm.stamps[jb.vidx][jb.rank];
+            stt.timely = stt.contrib_stamp == jb.version;
+            stt.activator = jb.vidx >= 0 ? sm.activator[jb.vidx] : 0;
+            stt.error = int32_t(ld_relaxed_sys(err_ptr(p)));
+            stt.pad = 0;
+            p.status[tid] = stt;
+        }
+    }
+}
+
 __global__ void fill_i64_kernel(int64_t* p, int64_t n, int64_t v) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) p[i] = v;
 }
@@ -1400,7 +1924,9 @@ struct wg_ctx {
     long long* prof;
     int fence_scope;
     int use_nvl;
+    int use_split;
     int occ_nvl[2];
+    int occ_split[2];
 };
 
 extern "C" {
@@ -1465,6 +1991,11 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     off = align_up(off + int64_t(ctx->R) * ctx->n_tiles * kWarps * 8, 4096);
     L.ring = off;
     off = align_up(off + int64_t(ctx->R) * ctx->D * ctx->npad * int64_t(ctx->esize), 4096);
+    const int64_t red = (c.n_gpus >= 4 && c.P <= kSplitMaxP) ? 1 : 0;  // split sums pay off across >= 4 GPUs
+    L.red_flags = off;
+    off = align_up(off + red * int64_t(ctx->R) * ctx->n_tiles * 8, 4096);
+    L.red_ring = off;
+    off = align_up(off + red * int64_t(ctx->R) * ctx->D * ctx->npad * int64_t(ctx->esize), 4096);
     L.total = off;
 
     int rc = WG_OK;
@@ -1482,6 +2013,7 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
         fill(L.announce, int64_t(ctx->R) * kAnnounceStride, -1);
         fill(L.complete, int64_t(ctx->R) * ctx->D, kNever);
         fill(L.flags, int64_t(ctx->R) * ctx->n_tiles * kWarps, kNever);
+        if (L.red_ring > L.red_flags) fill(L.red_flags, int64_t(ctx->R) * ctx->n_tiles, kNever);
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "arena init: %s", cudaGetErrorString(e)); break; }
         e = cudaHostAlloc(&ctx->status_host, sizeof(wg_job_status) * kMaxJobs, cudaHostAllocMapped);
@@ -1501,6 +2033,10 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
             e = cudaFuncSetAttribute(wagma_nvl_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNvlMaxDyn);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(wagma_nvl_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNvlMaxDyn);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(wagma_split_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNvlMaxDyn);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(wagma_split_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNvlMaxDyn);
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)); break; }
         e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, c.device);
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "device attribute: %s", cudaGetErrorString(e)); break; }
@@ -1515,6 +2051,8 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     ctx->opened[c.gpu_index] = false;
     ctx->use_nvl = 1;
     if (const char* nv = getenv("WG_NVL")) ctx->use_nvl = atoi(nv);
+    ctx->use_split = 1;
+    if (const char* sp = getenv("WG_SPLIT")) ctx->use_split = atoi(sp);
     ctx->fence_scope = 1;  // GPU scope for per-tile flags (see publish_tile)
     if (const char* fs = getenv("WG_FENCE_SCOPE")) {
         if (!strcmp(fs, "sys")) ctx->fence_scope = 0;
@@ -1799,6 +2337,12 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
             P_.log_leaves = ilog2(nl);
             P_.divisor = sync ? c.P : c.S;
             P_.divisor_pow2 = is_pow2(P_.divisor);
+            int own[kMaxLeaves], no = 0;
+            for (int i = 0; i < nl; ++i) own[no++] = leaves[i];
+            std::sort(own, own + no);
+            no = int(std::unique(own, own + no) - own);
+            P_.n_owners = no;
+            for (int i = 0; i < no; ++i) P_.owners[i] = int16_t(own[i]);
             P_.n_members = 0;
             for (int i = 0; i < nl; ++i) P_.leaves[i] = int16_t(leaves[i]);
         }
@@ -1841,7 +2385,47 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
     const int nvl_stages =
         n_rows == 0 ? kNvlMaxStages
                     : int(std::min<size_t>(kNvlMaxStages, (size_t(kNvlMaxDyn) - nvl_fixed) / (size_t(n_rows) * row)));
-    if (p.need_fence && ctx->use_nvl && nvl_stages >= 2 && n_leaves_total * kWarps <= kMaxPoll &&
+    bool wide = false;  // some group of this launch spans >= 4 GPUs (same answer on every GPU)
+    for (int k = 0; k < p.n_plans; ++k) {
+        unsigned gpus = 0;
+        for (int li = 0; li < p.plans[k].n_leaves; ++li) gpus |= 1u << (p.plans[k].leaves[li] / ctx->R);
+        wide = wide || (__builtin_popcount(gpus) >= 4 && p.plans[k].n_owners == p.plans[k].n_leaves);
+    }
+    if (p.need_fence && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= 4 && wide) {
+        // split sums: every GPU of a job makes this same choice (it depends on
+        // P and the process-wide knob only), so owners always publish the
+        // reduced tiles their peers wait for
+        // stream B (1 row per plan) gets what stream A (all leaves) leaves
+        // after 4 stages, between 2 and 16 stages each
+        const size_t rowsA = size_t(std::max(n_leaves_total, 1)) * row, rowsB = size_t(p.n_plans) * row;
+        const size_t avail = size_t(kNvlMaxDyn) > nvl_fixed ? size_t(kNvlMaxDyn) - nvl_fixed : 0;
+        const int nsb = int(std::max<size_t>(
+            2, std::min<size_t>(kNvlMaxStages, avail > 4 * rowsA ? (avail - 4 * rowsA) / rowsB : 0)));
+        const size_t fixed = nvl_fixed + size_t(nsb) * rowsB;
+        const int nsa = fixed >= size_t(kNvlMaxDyn)
+                            ? 0
+                            : int(std::min<size_t>(kNvlMaxStages, (size_t(kNvlMaxDyn) - fixed) / rowsA));
+        if (nsa < 2 || n_leaves_total * kWarps > kMaxPoll)
+            return fail(WG_EINVAL, "split launch does not fit shared memory (%d leaves)", n_leaves_total);
+        p.nvl_stages = nsa;
+        p.split_stages = nsb;
+        const size_t smem_split = fixed + size_t(nsa) * n_leaves_total * row;
+        const int di = c.dtype == WG_F32 ? 0 : 1;
+        if (ctx->occ_split[di] <= 0) {
+            int o = 0;
+            cudaError_t e2 = c.dtype == WG_F32
+                                 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wagma_split_kernel<float>,
+                                                                                 kSplitThreads, kNvlMaxDyn)
+                                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wagma_split_kernel<double>,
+                                                                                 kSplitThreads, kNvlMaxDyn);
+            ctx->occ_split[di] = (e2 == cudaSuccess && o > 0) ? o : 1;
+        }
+        const int64_t g = std::min<int64_t>(ctx->n_tiles, int64_t(ctx->occ_split[di]) * ctx->sms);
+        if (c.dtype == WG_F32)
+            wagma_split_kernel<float><<<unsigned(g), kSplitThreads, smem_split, s>>>(p);
+        else
+            wagma_split_kernel<double><<<unsigned(g), kSplitThreads, smem_split, s>>>(p);
+    } else if (p.need_fence && ctx->use_nvl && nvl_stages >= 2 && n_leaves_total * kWarps <= kMaxPoll &&
         n_leaves_total <= kMaxPlans * kMaxLeaves) {
         p.nvl_stages = nvl_stages;
         const size_t nvl_smem = nvl_fixed + size_t(nvl_stages) * n_rows * row;

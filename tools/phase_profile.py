@@ -49,7 +49,9 @@ for t in range(a.iters):
     t = t * 8 + 7
     if True:
         p = prof.view(-1, 8).cpu().numpy().astype(np.float64)
-        if os.environ.get("WG_NVL", "1") != "0":
+        if os.environ.get("WG_PROF_SPLIT", "0") == "1":
+            names = ["producer_total", "pullA_total", "x", "redA_full_wait", "redA_total", "pullB_total", "finB_full_wait", "finB_total"]
+        elif os.environ.get("WG_NVL", "1") != "0":
             names = ["producer_total", "pull_empty_wait", "pull_poll", "pull_issue", "cons_full_wait", "x", "cons_total", "cons_ready_wait"]
         else:
             names = ["produce", "publish", "resolve", "poll", "consume", "tiles", "fence"]
