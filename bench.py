@@ -201,30 +201,41 @@ def step_bytes(a, G, gpu_index, t, elem):
     """(HBM bytes, NVLink ingress bytes) one launch on `gpu_index` must move.
 
     Own streams per local rank: read W, m, g; write m, the send-slot W' and
-    W_{t+1} = 6 * elem * n. Each leaf of a group sum living on another GPU
-    crosses NVLink once (ingress here) and is read from the owner's HBM (by
-    symmetry the same count is served from this GPU's HBM).
+    W_{t+1} = 6 * elem * n. Pulled group sum: each leaf on another GPU
+    crosses NVLink once. Split group sum (all-timely group spanning >= 4
+    GPUs, P <= 8; the kernel's rule): a fraction f = L/S of the tiles is
+    reduced here (S - L remote leaves each, local leaves re-read, the reduced
+    tile written), the rest arrive as one reduced tile from their owner.
+    Bytes read from this GPU by peers (symmetric) are added to its HBM.
     """
     from paper_2005_00124_b200.topology import GroupingParams, compute_groups, tree_leaves
     R = a.P // G
     local = range(gpu_index * R, (gpu_index + 1) * R)
-    own = R * 6 * elem * a.n
+    n = elem * a.n
+    hbm = R * 6 * n
+    nvl = 0.0
     sync = (t + 1) % a.tau == 0
-    remote_leaves = 0
-    if sync:
-        remote_leaves = a.P - R  # one global plan per GPU
-    else:
+    split_on = os.environ.get("WG_SPLIT", "1") != "0" and G >= 4 and a.P <= 8
+    groups = [tuple(range(a.P))] if sync else None
+    if not sync:
         part = compute_groups(GroupingParams(a.P, a.S, t))
-        seen = set()
+        groups = []
         for r in local:
             grp = part.group_of(r)
-            if grp in seen:
-                continue
-            seen.add(grp)
-            leaves = tree_leaves(GroupingParams(a.P, a.S, t), grp[0])
-            remote_leaves += sum(1 for q in leaves if q // R != gpu_index)
-    nvl = remote_leaves * elem * a.n
-    return own + nvl, nvl
+            if grp not in groups:
+                groups.append(grp)
+    for grp in groups:
+        leaves = grp if sync else tree_leaves(GroupingParams(a.P, a.S, t), grp[0])
+        L = sum(1 for q in grp if q // R == gpu_index)
+        S = len(grp)
+        spans = len({q // R for q in grp})
+        if split_on and spans >= 4 and len(set(leaves)) == len(leaves):
+            f = L / S
+            nvl += n * (f * (S - L) + (1 - f))
+            hbm += n * f * (L + 1)
+        else:
+            nvl += n * sum(1 for q in leaves if q // R != gpu_index)
+    return hbm + nvl, nvl
 
 
 def load_traffic(a, G):

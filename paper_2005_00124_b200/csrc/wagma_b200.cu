@@ -115,10 +115,14 @@ struct DevVersion {
 
 struct DevPlan {
     int32_t vidx, n_leaves, log_leaves, divisor, n_members, divisor_pow2;
-    int32_t n_owners, pad;          // distinct group members (split-sum owners)
     int16_t leaves[kMaxLeaves];
-    int16_t owners[kMaxLeaves];     // sorted distinct members (split-sum owners, see split_owner)
     int8_t members[kMaxJobs];
+};
+
+// Split-sum owners of a plan: its sorted distinct members (see split_owner).
+struct DevOwners {
+    int32_t n;
+    int16_t rank[kMaxLeaves];
 };
 
 struct LaunchParams {
@@ -132,6 +136,7 @@ struct LaunchParams {
     DevVersion versions[kMaxVersions];
     DevPlan plans[kMaxPlans];
     int64_t forced[kMaxVersions][kMaxP];
+    DevOwners owners[kMaxPlans];
     wg_job_status* status;
     long long* prof;  // optional per-CTA phase cycle counters [grid][8]
     int32_t fence_scope;  // 0 sys, 1 gpu (default), 2 none (timing experiments only)
@@ -433,7 +438,6 @@ struct SmemCtl {
     int8_t leaf_src[kMaxPlans][kMaxLeaves];  // >=0: stage of job; -1 poll; -2 ready
     int16_t leaf_slot[kMaxPlans][kMaxLeaves];
     int32_t plan_polls[kMaxPlans];
-    int32_t plan_split[kMaxPlans];
     int32_t activator[kMaxVersions];
     int32_t abort;
 };
@@ -1404,8 +1408,8 @@ constexpr int kFinThreads = 4 * 32;
 // Owner of a tile of a split sum: rotates along each CTA's tile sequence so
 // every CTA reduces 1/n_owners of its tiles (tile t is the (t / grid)-th tile
 // of CTA t % grid; the grid is identical on every GPU).
-__device__ __forceinline__ int split_owner(const DevPlan& P_, int64_t tile) {
-    return P_.owners[(tile / gridDim.x) % P_.n_owners];
+__device__ __forceinline__ int split_owner(const LaunchParams& p, int pl, int64_t tile) {
+    return p.owners[pl].rank[(tile / gridDim.x) % p.owners[pl].n];
 }
 
 template <typename T>
@@ -1430,6 +1434,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     __shared__ unsigned bt_mask[kPullBatch];
     __shared__ int bt_n;
     __shared__ int cell_pref[kPullBatch * kMaxPlans + 1];
+    __shared__ int plan_split[kMaxPlans];
     __shared__ int64_t btB_tile[kPullBatch];
     __shared__ unsigned btB_mask[kPullBatch];
     __shared__ int btB_n;
@@ -1470,7 +1475,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         ma = mb = 0;
         for (int pl = 0; pl < NP; ++pl) {
             const DevPlan& P_ = p.plans[pl];
-            const bool remote_owner = sm.plan_split[pl] && split_owner(P_, tile) / p.R != p.gpu_index;
+            const bool remote_owner = plan_split[pl] && split_owner(p, pl, tile) / p.R != p.gpu_index;
             (remote_owner ? mb : ma) |= 1u << pl;
         }
     };
@@ -1502,7 +1507,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 plan_poll_base[pl] = n_poll;
                 // split when every member is timely and the group spans >= 4
                 // GPUs (fewer: the reduced-tile copies save little NVLink)
-                bool split = P_.n_owners == P_.n_leaves && P_.n_owners >= 2;
+                bool split = p.owners[pl].n == P_.n_leaves && p.owners[pl].n >= 2;
                 bool remote = false;
                 unsigned gpus = 0;
                 for (int li = 0; li < P_.n_leaves; ++li) {
@@ -1528,7 +1533,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                     }
                 }
                 plan_poll_cnt[pl] = n_poll - plan_poll_base[pl];
-                sm.plan_split[pl] = split && remote;
+                plan_split[pl] = split && remote;
             }
             __threadfence_block();
             ready = aborted(p) ? 2 : 1;
@@ -1674,8 +1679,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 const int base = leaf_base[pl];
                 auto fetch = [&](int leaf) -> V { return lb[(base + leaf) * kThreads + ctid]; };
                 const V acc = tree_sum<T>(fetch, P_.log_leaves);
-                if (sm.plan_split[pl]) {  // this GPU owns the tile: publish the reduced tile
-                    __stcg(reinterpret_cast<V*>(red_ptr<T>(p, split_owner(P_, tile),
+                if (plan_split[pl]) {  // this GPU owns the tile: publish the reduced tile
+                    __stcg(reinterpret_cast<V*>(red_ptr<T>(p, split_owner(p, pl, tile),
                                                           p.versions[P_.vidx].version) + idx), acc);
                     owned = true;
                 }
@@ -1703,9 +1708,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                         fence_sys();
                     else
                         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    if (lane < NP && (mask >> lane & 1) && sm.plan_split[lane]) {
+                    if (lane < NP && (mask >> lane & 1) && plan_split[lane]) {
                         const DevPlan& P_ = p.plans[lane];
-                        st_relaxed_sys(red_flag_ptr(p, split_owner(P_, tile), tile),
+                        st_relaxed_sys(red_flag_ptr(p, split_owner(p, lane, tile), tile),
                                        p.versions[P_.vidx].version);
                     }
                 }
@@ -1753,7 +1758,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             if (e < nb * NP && (btB_mask[e / NP] >> (e % NP) & 1)) {
                 const DevPlan& P_ = p.plans[e % NP];
                 want = p.versions[P_.vidx].version;
-                fp = red_flag_ptr(p, split_owner(P_, btB_tile[e / NP]), btB_tile[e / NP]);
+                fp = red_flag_ptr(p, split_owner(p, e % NP, btB_tile[e / NP]), btB_tile[e / NP]);
                 x = ld_relaxed_sys(fp);
             }
             int rc = 0;
@@ -1796,7 +1801,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 __syncwarp();
                 if (lane < NP && (mb >> lane & 1)) {
                     const DevPlan& P_ = p.plans[lane];
-                    const T* src = red_ptr<T>(p, split_owner(P_, tile), p.versions[P_.vidx].version) +
+                    const T* src = red_ptr<T>(p, split_owner(p, lane, tile), p.versions[P_.vidx].version) +
                                    tile * p.tile_elems;
                     bulk_g2s(ringB + (size_t(st) * NP + lane) * kThreads, src, tile_bytes, &fullB[st]);
                 }
@@ -2341,8 +2346,8 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
             for (int i = 0; i < nl; ++i) own[no++] = leaves[i];
             std::sort(own, own + no);
             no = int(std::unique(own, own + no) - own);
-            P_.n_owners = no;
-            for (int i = 0; i < no; ++i) P_.owners[i] = int16_t(own[i]);
+            p.owners[pl].n = no;
+            for (int i = 0; i < no; ++i) p.owners[pl].rank[i] = int16_t(own[i]);
             P_.n_members = 0;
             for (int i = 0; i < nl; ++i) P_.leaves[i] = int16_t(leaves[i]);
         }
@@ -2389,7 +2394,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
     for (int k = 0; k < p.n_plans; ++k) {
         unsigned gpus = 0;
         for (int li = 0; li < p.plans[k].n_leaves; ++li) gpus |= 1u << (p.plans[k].leaves[li] / ctx->R);
-        wide = wide || (__builtin_popcount(gpus) >= 4 && p.plans[k].n_owners == p.plans[k].n_leaves);
+        wide = wide || (__builtin_popcount(gpus) >= 4 && p.owners[k].n == p.plans[k].n_leaves);
     }
     if (p.need_fence && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= 4 && wide) {
         // split sums: every GPU of a job makes this same choice (it depends on
