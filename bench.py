@@ -202,8 +202,8 @@ def step_bytes(a, G, gpu_index, t, elem):
 
     Own streams per local rank: read W, m, g; write m, the send-slot W' and
     W_{t+1} = 6 * elem * n. Pulled group sum: each leaf on another GPU
-    crosses NVLink once. Split group sum (all-timely group spanning >= 4
-    GPUs, P <= 8; the kernel's rule): a fraction f = L/S of the tiles is
+    crosses NVLink once. Split group sum (all-timely group over >= 2 GPUs
+    where it saves bytes, P <= 8; the kernel's split_pays): a fraction f = L/S of the tiles is
     reduced here (S - L remote leaves each, local leaves re-read, the reduced
     tile written), the rest arrive as one reduced tile from their owner.
     Bytes read from this GPU by peers (symmetric) are added to its HBM.
@@ -215,7 +215,7 @@ def step_bytes(a, G, gpu_index, t, elem):
     hbm = R * 6 * n
     nvl = 0.0
     sync = (t + 1) % a.tau == 0
-    split_on = os.environ.get("WG_SPLIT", "1") != "0" and G >= 4 and a.P <= 8
+    split_on = os.environ.get("WG_SPLIT", "1") != "0" and G >= 2 and a.P <= 8
     groups = [tuple(range(a.P))] if sync else None
     if not sync:
         part = compute_groups(GroupingParams(a.P, a.S, t))
@@ -229,7 +229,8 @@ def step_bytes(a, G, gpu_index, t, elem):
         L = sum(1 for q in grp if q // R == gpu_index)
         S = len(grp)
         spans = len({q // R for q in grp})
-        if split_on and spans >= 4 and len(set(leaves)) == len(leaves):
+        if split_on and spans >= int(os.environ.get("WG_SPLIT_SPAN", "2")) and 2 * S >= 3 * (S // spans + 1) and \
+                len(set(leaves)) == len(leaves):
             f = L / S
             nvl += n * (f * (S - L) + (1 - f))
             hbm += n * f * (L + 1)

@@ -92,6 +92,10 @@ struct Layout {
 constexpr int kAnnounceStride = 16;  // int64 words (128 B)
 constexpr int kWarps = kThreads / 32;
 constexpr int kSplitMaxP = 8;  // split sums (reduce-scatter + all-gather) up to this many ranks
+// A split sum of S members spread over `span` GPUs (L = S/span per GPU) moves
+// (L/S)(S-L) + (1 - L/S) leaf-tiles over NVLink per tile against S - L for
+// the pull; split when that saves at least a third: 2S >= 3(L + 1).
+__host__ __device__ constexpr bool split_pays(int S, int span) { return 2 * S >= 3 * (S / span + 1); }
 constexpr int64_t kNever = INT64_MIN / 2;
 
 enum VersionMode : int32_t { kLive = 0, kForced = 1, kBlocking = 2, kSync = 3 };
@@ -142,7 +146,7 @@ struct LaunchParams {
     int32_t fence_scope;  // 0 sys, 1 gpu (default), 2 none (timing experiments only)
     int32_t nvl_stages;   // leaf-ring stages of the multi-GPU TMA kernel
     int32_t split_stages; // reduced-tile ring stages of the split kernel
-    int32_t pad3;
+    int32_t split_span;   // minimum GPUs a group must span to be summed split
 };
 
 // ---------------------------------------------------------------------------
@@ -1505,8 +1509,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 const DevPlan& P_ = p.plans[pl];
                 const int64_t v = p.versions[P_.vidx].version;
                 plan_poll_base[pl] = n_poll;
-                // split when every member is timely and the group spans >= 4
-                // GPUs (fewer: the reduced-tile copies save little NVLink)
+                // split when every member is timely, the group spans several GPUs
+                // and the split saves NVLink bytes (split_pays)
                 bool split = p.owners[pl].n == P_.n_leaves && p.owners[pl].n >= 2;
                 bool remote = false;
                 unsigned gpus = 0;
@@ -1516,7 +1520,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                     remote = remote || q / p.R != p.gpu_index;
                     gpus |= 1u << (q / p.R);
                 }
-                split = split && __popc(gpus) >= 4;
+                split = split && __popc(gpus) >= p.split_span && split_pays(p.owners[pl].n, __popc(gpus));
                 for (int li = 0; li < P_.n_leaves; ++li) {
                     const int q = P_.leaves[li];
                     if (sm.leaf_src[pl][li] == kSrcReady) continue;
@@ -1930,6 +1934,7 @@ struct wg_ctx {
     int fence_scope;
     int use_nvl;
     int use_split;
+    int split_span;
     int occ_nvl[2];
     int occ_split[2];
 };
@@ -1970,6 +1975,18 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     if (ctx->cfg.grace_ns <= 0) ctx->cfg.grace_ns = 100000;
     if (ctx->cfg.timeout_ns <= 0) ctx->cfg.timeout_ns = 20000000000ll;
     ctx->R = c.P / c.n_gpus;
+    // process-wide knobs (environment; identical on every process of a job)
+    ctx->use_nvl = 1;
+    if (const char* nv = getenv("WG_NVL")) ctx->use_nvl = atoi(nv);
+    ctx->use_split = 1;
+    if (const char* sp = getenv("WG_SPLIT")) ctx->use_split = atoi(sp);
+    ctx->split_span = 2;  // the same on every process of a job (environment knob for experiments)
+    if (const char* ss = getenv("WG_SPLIT_SPAN")) ctx->split_span = std::max(2, atoi(ss));
+    ctx->fence_scope = 1;  // GPU scope for per-tile flags (see publish_tile)
+    if (const char* fs = getenv("WG_FENCE_SCOPE")) {
+        if (!strcmp(fs, "sys")) ctx->fence_scope = 0;
+        if (!strcmp(fs, "none")) ctx->fence_scope = 2;  // timing experiments only: unsafe
+    }
     ctx->D = c.ring_depth > 0 ? c.ring_depth : (c.tau > 0 ? int(std::max<int64_t>(2 * c.tau, 4)) : 16);
     ctx->Dv = c.version_ring > 0 ? c.version_ring : (c.tau > 0 ? int(std::max<int64_t>(2 * c.tau, 8)) : 64);
     if (ctx->D < 2 || ctx->D > 32767) {
@@ -1996,7 +2013,7 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     off = align_up(off + int64_t(ctx->R) * ctx->n_tiles * kWarps * 8, 4096);
     L.ring = off;
     off = align_up(off + int64_t(ctx->R) * ctx->D * ctx->npad * int64_t(ctx->esize), 4096);
-    const int64_t red = (c.n_gpus >= 4 && c.P <= kSplitMaxP) ? 1 : 0;  // split sums pay off across >= 4 GPUs
+    const int64_t red = (ctx->use_split && c.n_gpus >= ctx->split_span && c.P <= kSplitMaxP) ? 1 : 0;
     L.red_flags = off;
     off = align_up(off + red * int64_t(ctx->R) * ctx->n_tiles * 8, 4096);
     L.red_ring = off;
@@ -2054,15 +2071,6 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     }
     ctx->base[c.gpu_index] = ctx->arena;
     ctx->opened[c.gpu_index] = false;
-    ctx->use_nvl = 1;
-    if (const char* nv = getenv("WG_NVL")) ctx->use_nvl = atoi(nv);
-    ctx->use_split = 1;
-    if (const char* sp = getenv("WG_SPLIT")) ctx->use_split = atoi(sp);
-    ctx->fence_scope = 1;  // GPU scope for per-tile flags (see publish_tile)
-    if (const char* fs = getenv("WG_FENCE_SCOPE")) {
-        if (!strcmp(fs, "sys")) ctx->fence_scope = 0;
-        if (!strcmp(fs, "none")) ctx->fence_scope = 2;  // timing experiments only: unsafe
-    }
     *out = ctx;
     return WG_OK;
 }
@@ -2228,6 +2236,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
     p.status = ctx->status_dev;
     p.prof = ctx->prof;
     p.fence_scope = ctx->fence_scope;
+    p.split_span = ctx->split_span;
     for (int q = 0; q < kMaxP; ++q) p.job_of_rank[q] = -1;
 
     const size_t align_mask = 15;
@@ -2394,9 +2403,10 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
     for (int k = 0; k < p.n_plans; ++k) {
         unsigned gpus = 0;
         for (int li = 0; li < p.plans[k].n_leaves; ++li) gpus |= 1u << (p.plans[k].leaves[li] / ctx->R);
-        wide = wide || (__builtin_popcount(gpus) >= 4 && p.owners[k].n == p.plans[k].n_leaves);
+        wide = wide || (__builtin_popcount(gpus) >= ctx->split_span && p.owners[k].n == p.plans[k].n_leaves &&
+                        split_pays(p.owners[k].n, __builtin_popcount(gpus)));
     }
-    if (p.need_fence && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= 4 && wide) {
+    if (p.need_fence && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= ctx->split_span && wide) {
         // split sums: every GPU of a job makes this same choice (it depends on
         // P and the process-wide knob only), so owners always publish the
         // reduced tiles their peers wait for
