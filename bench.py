@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--victims", type=int, default=0, help="StragglerPolicy victims per iteration")
     ap.add_argument("--extra-ms", type=float, default=0.0, help="extra delay of a victim rank's GPU")
     ap.add_argument("--straggler-seed", type=int, default=12)
+    ap.add_argument("--length-buckets", action="store_true",
+                    help="C3: per-(rank, t) compute time base_ms * L / mean(L), L from WMT-style length buckets")
     return ap.parse_args()
 
 
@@ -292,9 +294,12 @@ def run_ours(a):
     from paper_2005_00124_b200.straggler import StragglerPolicy
     policy = StragglerPolicy(a.victims, a.extra_ms, selection_seed=a.straggler_seed) if a.victims else None
 
+    from paper_2005_00124_b200.straggler import BucketedLengthDelay
+    lengths = BucketedLengthDelay(a.base_ms, seed=a.straggler_seed) if a.length_buckets else None
+
     def delay(t):
         """compute_delay (netsim.py:103-117) as a device spin before this GPU's step."""
-        ms = a.base_ms
+        ms = a.base_ms if lengths is None else max(lengths.delay_ms(r, t) for r in local)
         if policy is not None and set(local) & policy.victims(t, a.P):
             ms += a.extra_ms
         if ms > 0:
@@ -439,7 +444,7 @@ def run_ours(a):
                 "vs_baseline": None, "dtype": a.dtype, "data": "synthetic", "config": config_dict(a, G),
                 "group_avg_gbs": group_avg_gbs, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": gpu_launches, "clocks": clocks}
-        if a.blocking or a.victims or a.base_ms:
+        if a.blocking or a.victims or a.base_ms or a.length_buckets:
             from paper_2005_00124_b200.optim import is_sync_iteration
             stale = total = 0
             for v in range(max(0, t - ctx.ring_depth + 1), t):
@@ -452,6 +457,8 @@ def run_ours(a):
             line["imbalance"] = {"activation": "blocking (beta)" if a.blocking else "wait-avoiding (alpha)",
                                  "base_ms": a.base_ms, "victims_per_iteration": a.victims, "extra_ms": a.extra_ms,
                                  "selection_seed": a.straggler_seed,
+                                 "delay_model": "bucketed sequence lengths (WMT-style)" if a.length_buckets
+                                 else "base + victims",
                                  "stale_contribution_fraction": (stale / total) if total else None}
             line["config"]["activation"] = line["imbalance"]["activation"]
         print(json.dumps(line), flush=True)

@@ -1004,6 +1004,13 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
 #define WG_NVL_TMA_LOCAL 1
 #endif
 constexpr int kNvlDepth = WG_NVL_DEPTH;  // producer cp.async ring depth (items)
+#ifndef WG_SPLIT_DEPTH
+#define WG_SPLIT_DEPTH 3
+#endif
+#ifndef WG_SPLIT_NSB
+#define WG_SPLIT_NSB 16
+#endif
+constexpr int kSplitDepth = WG_SPLIT_DEPTH;  // producer ring depth in the split kernel
 constexpr int kNvlMaxStages = 16;
 constexpr int kNvlThreads = 2 * kThreads + 32;
 constexpr int kNvlMaxDyn = 200 * 1024;
@@ -1064,7 +1071,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // readiness flags published in chunks of kPubChunk by the last warp to
 // finish a chunk (one GPU-scope fence, cumulative over the other warps'
 // stores acquired through the shared-memory counter). Never waits on a peer.
-template <typename T>
+template <typename T, int kNvlDepth>
 __device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename Tr<T>::V* ring, int64_t my_ntiles,
                                                 unsigned* pub_count) {
     using V = typename Tr<T>::V;
@@ -1196,7 +1203,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     if (warp < kWarps) {
         // ---------------- producers ----------------
         const long long pc0 = clock64();
-        my_tiles = nvl_produce<T>(p, ring, my_ntiles, pub_count);
+        my_tiles = nvl_produce<T, kNvlDepth>(p, ring, my_ntiles, pub_count);
         if (p.prof && tid == 0) p.prof[blockIdx.x * 8 + 0] = clock64() - pc0;
     } else if (warp == 2 * kWarps) {
         // ---------------- puller ----------------
@@ -1470,7 +1477,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     const int NL = leaf_base[NP];
     V* ringA = reinterpret_cast<V*>(dyn_smem);              // [NSA][NL][kThreads]
     V* ringB = ringA + size_t(NSA) * NL * kThreads;           // [NSB][NP][kThreads]
-    V* ring = ringB + size_t(NSB) * NP * kThreads;            // [kNvlDepth][3][kThreads]
+    V* ring = ringB + size_t(NSB) * NP * kThreads;            // [kSplitDepth][3][kThreads]
     const int64_t my_ntiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const unsigned tile_bytes = unsigned(p.tile_elems * int64_t(sizeof(T)));
     unsigned my_tiles = 0;
@@ -1496,7 +1503,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         if (p.prof) p.prof[blockIdx.x * 8 + slot] = v;
     };
     if (warp < kWarps) {
-        my_tiles = nvl_produce<T>(p, ring, my_ntiles, pub_count);
+        my_tiles = nvl_produce<T, kSplitDepth>(p, ring, my_ntiles, pub_count);
         if (tid == 0) prof_set(0, clock64() - t_start);
     } else if (warp == kWarps) {
         // ---------------- stream A puller ----------------
@@ -2413,10 +2420,11 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         // stream B (1 row per plan) gets what stream A (all leaves) leaves
         // after 4 stages, between 2 and 16 stages each
         const size_t rowsA = size_t(std::max(n_leaves_total, 1)) * row, rowsB = size_t(p.n_plans) * row;
-        const size_t avail = size_t(kNvlMaxDyn) > nvl_fixed ? size_t(kNvlMaxDyn) - nvl_fixed : 0;
+        const size_t split_fixed = size_t(kSplitDepth * 3) * row;
+        const size_t avail = size_t(kNvlMaxDyn) > split_fixed ? size_t(kNvlMaxDyn) - split_fixed : 0;
         const int nsb = int(std::max<size_t>(
-            2, std::min<size_t>(kNvlMaxStages, avail > 4 * rowsA ? (avail - 4 * rowsA) / rowsB : 0)));
-        const size_t fixed = nvl_fixed + size_t(nsb) * rowsB;
+            2, std::min<size_t>(WG_SPLIT_NSB, avail > 4 * rowsA ? (avail - 4 * rowsA) / rowsB : 0)));
+        const size_t fixed = split_fixed + size_t(nsb) * rowsB;
         const int nsa = fixed >= size_t(kNvlMaxDyn)
                             ? 0
                             : int(std::min<size_t>(kNvlMaxStages, (size_t(kNvlMaxDyn) - fixed) / rowsA));

@@ -15,7 +15,7 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["StragglerPolicy", "DelayModel", "compute_delay"]
+__all__ = ["StragglerPolicy", "DelayModel", "compute_delay", "BucketedLengthDelay", "WMT_BUCKETS"]
 
 
 @dataclass(frozen=True)
@@ -61,3 +61,37 @@ def compute_delay(proc: int, iteration: int, model: DelayModel, rng_seed: int, P
     if model.straggler is not None and proc in model.straggler.victims(iteration, P):
         delay += model.straggler.extra_delay_ms
     return delay
+
+
+# (sequence length, share of batches) -- a WMT-style length-bucketed batching
+# profile: most batches are short, a long tail of long ones.
+WMT_BUCKETS = ((16, 0.18), (24, 0.20), (32, 0.19), (48, 0.16), (64, 0.12), (96, 0.08), (128, 0.05),
+               (192, 0.015), (256, 0.005))
+
+
+@dataclass(frozen=True)
+class BucketedLengthDelay:
+    """Per-(rank, iteration) compute time from a bucketed sequence-length draw.
+
+    The imbalance of the Transformer experiment (arXiv 2005.00124 §6.2,
+    PAPER.md:795): every rank's batch holds sentences of one length bucket,
+    so its step time scales with the bucket's length. The reference only has
+    uniform jitter plus victims (netsim.py:85-117); this is the new delay
+    model SURVEY.md §8(d) asks for C3. Deterministic in (seed, iteration,
+    rank) through numpy's PCG64, like `compute_delay`'s jitter.
+    """
+
+    base_ms: float
+    buckets: tuple = WMT_BUCKETS
+    seed: int = 0
+
+    def mean_length(self) -> float:
+        tot = sum(p for _, p in self.buckets)
+        return sum(L * p for L, p in self.buckets) / tot
+
+    def delay_ms(self, rank: int, iteration: int) -> float:
+        rng = np.random.default_rng([self.seed, iteration, rank])
+        lengths = np.array([L for L, _ in self.buckets], dtype=np.float64)
+        probs = np.array([p for _, p in self.buckets], dtype=np.float64)
+        L = float(rng.choice(lengths, p=probs / probs.sum()))
+        return self.base_ms * L / self.mean_length()

@@ -1,0 +1,94 @@
+"""Host-side logic of the drop-in modules (CPU only).
+
+StragglerPolicy / compute_delay against the reference's own victim draws
+(tests/golden/topology.json), the new length-bucket delay model, the
+configuration API restated from the reference's optimizer tests
+(`pkg/tests/test_optim.py:103-161`), and the launch-tick straggler emulation.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from paper_2005_00124_b200.driver import TickSchedule
+from paper_2005_00124_b200.optim import ConfigError, EtaSchedule, OptimizerConfig, is_sync_iteration
+from paper_2005_00124_b200.straggler import (
+    BucketedLengthDelay,
+    DelayModel,
+    StragglerPolicy,
+    compute_delay,
+)
+
+
+def test_victims_match_reference():
+    with open(os.path.join(GOLDEN, "topology.json")) as fp:
+        golden = json.load(fp)["victims"]
+    for seed, P, k, t, want in golden:
+        assert sorted(StragglerPolicy(k, 1.0, selection_seed=seed).victims(t, P)) == want
+
+
+def test_compute_delay_rules():
+    pol = StragglerPolicy(2, 320.0, selection_seed=3)
+    dm = DelayModel(base_compute_ms=100.0, jitter_max_ms=5.0, straggler=pol)
+    for t in range(6):
+        vict = pol.victims(t, 8)
+        for r in range(8):
+            d = compute_delay(r, t, dm, 11, 8)
+            assert d == compute_delay(r, t, dm, 11, 8)  # pure
+            extra = 320.0 if r in vict else 0.0
+            assert 100.0 + extra <= d <= 105.0 + extra
+    with pytest.raises(ValueError):
+        compute_delay(8, 0, dm, 11, 8)
+    with pytest.raises(ValueError):
+        StragglerPolicy(9, 1.0).victims(0, 8)
+    with pytest.raises(ValueError):
+        DelayModel(base_compute_ms=-1.0)
+
+
+def test_bucketed_length_delay():
+    d = BucketedLengthDelay(2.0, seed=7)
+    draws = np.array([d.delay_ms(r, t) for t in range(400) for r in range(8)])
+    assert draws.min() > 0 and draws.max() <= 2.0 * 256 / d.mean_length() + 1e-12
+    assert abs(draws.mean() - 2.0) < 0.15  # mean compute time = base
+    assert d.delay_ms(3, 5) == BucketedLengthDelay(2.0, seed=7).delay_ms(3, 5)
+    assert len({round(x, 9) for x in draws}) > 3  # actually imbalanced
+
+
+def test_eta_and_config_known_answers():
+    sched = EtaSchedule(kind="step", value=0.8, decay_factor=0.5, decay_every=3)
+    assert [sched.rate(t, 4, 100) for t in (0, 2, 3, 6)] == [0.8, 0.8, 0.4, 0.2]
+    assert EtaSchedule(kind="theorem").rate(0, 16, 400) == 16 / 20.0
+    with pytest.raises(ConfigError):
+        EtaSchedule(kind="cosine").rate(0, 1, 1)
+    with pytest.raises(ConfigError):
+        EtaSchedule(kind="step", decay_every=0).rate(0, 1, 1)
+    for bad in (dict(alpha=True, beta=True), dict(T=0), dict(tau=0), dict(b=0), dict(update_rule="adam"),
+                dict(S=3), dict(S=16)):
+        kw = dict(T=10, S=4, tau=5)
+        kw.update(bad)
+        with pytest.raises(ConfigError):
+            OptimizerConfig(**kw).validate(8)
+    with pytest.raises(ConfigError):
+        OptimizerConfig(T=10, eta=EtaSchedule(value=0.0)).validate(8)
+    OptimizerConfig(T=10, S=4, tau=5).validate(8)
+    assert [t for t in range(12) if is_sync_iteration(t, 4)] == [3, 7, 11]
+    assert not is_sync_iteration(3, None)
+
+
+@pytest.mark.parametrize("P,T,tau,k,dt", [(8, 20, 5, 2, 1), (4, 17, 4, 1, 2), (8, 12, None, 1, 1)])
+def test_tick_schedule_properties(P, T, tau, k, dt):
+    pol = StragglerPolicy(k, 1.0, selection_seed=5)
+    sched = TickSchedule(P, T, tau, lambda t: pol.victims(t, P), delay_ticks=dt)
+    done = {r: [] for r in range(P)}
+    for versions in sched.ticks():
+        assert len(versions) <= P
+        sync_ts = {t for t in versions.values() if is_sync_iteration(t, tau)}
+        if sync_ts:  # a global sync launches all ranks together at one version
+            assert len(versions) == P and len(set(versions.values())) == 1
+        for r, t in versions.items():
+            done[r].append(t)
+    for r in range(P):
+        assert done[r] == list(range(T))  # every rank runs every iteration once, in order
