@@ -428,10 +428,21 @@ def run_ours(a):
                        "(H2D and D2H on two copy streams, overlapped across steps)"}
         ctx.check()
 
-    # sanity: replicas finite
+    # sanity (untimed): replicas finite; run on to the next global sync and
+    # check the replicas are bit-identical there (optim.py:289-293)
     for r in local:
         if not torch.isfinite(opt.W[r]).all():
             raise SystemExit(f"non-finite replica on rank {r}")
+    from paper_2005_00124_b200.diagnostics import replica_diagnostics
+    while (t + 1) % a.tau != 0:
+        delay(t)
+        opt.step(t, {r: gpool[r][t % 2] for r in local})
+        t += 1
+    delay(t)
+    opt.step(t, {r: gpool[r][t % 2] for r in local})
+    t += 1
+    diag = replica_diagnostics(ctx, opt.W)
+    ctx.check()
 
     cpu = None
     if rank == 0 and G == 1 and not a.no_cpu:
@@ -443,7 +454,8 @@ def run_ours(a):
                 "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": a.dtype, "data": "synthetic", "config": config_dict(a, G),
                 "group_avg_gbs": group_avg_gbs, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": gpu_launches, "clocks": clocks}
+                "gpu_launches": gpu_launches, "clocks": clocks,
+                "replicas_after_sync": {"iteration": t - 1, "bit_identical": diag.identical, "gamma": diag.gamma}}
         if a.blocking or a.victims or a.base_ms or a.length_buckets:
             from paper_2005_00124_b200.optim import is_sync_iteration
             stale = total = 0

@@ -184,6 +184,16 @@ int wg_ctx_clear_error(wg_ctx* ctx);
  * a device-side spin of `ns` nanoseconds on `stream`. */
 int wg_delay(wg_ctx* ctx, int64_t ns, void* stream);
 
+/* Replica diagnostics (compute_diagnostics, optim.py:199-210). wg_replicas_sum
+ * adds sum_r W_r (fp64) of R device replicas (n elements) into `sum`;
+ * wg_replicas_spread adds sum_r ||W_r - mu||^2 into out[0] and writes
+ * max |W_r - W_0| into out[1] (fp64 device scalars, zero them first). With
+ * the global mean mu (sum over every rank / P, all-reduced across
+ * processes) and the all-reduced out[0], this is the spread potential
+ * Gamma_t; out[1] == 0 is the bit-identity check after a global sync. */
+int wg_replicas_sum(wg_ctx* ctx, const void* const* W, int R, double* sum, void* stream);
+int wg_replicas_spread(wg_ctx* ctx, const void* const* W, int R, const double* mu, double* out, void* stream);
+
 /* Instrumentation: per-CTA phase cycle counters (long long [grid][8]:
  * produce, publish, resolve, poll, consume, tiles) written by every
  * multi-GPU launch while dev_buf is non-NULL. */

@@ -78,6 +78,8 @@ SIGNATURES = {
     "wg_ctx_error": (_I, [_VP, _PI, _PI64]),
     "wg_ctx_clear_error": (_I, [_VP]),
     "wg_delay": (_I, [_VP, _I64, _VP]),
+    "wg_replicas_sum": (_I, [_VP, ctypes.POINTER(_VP), _I, _VP, _VP]),
+    "wg_replicas_spread": (_I, [_VP, ctypes.POINTER(_VP), _I, _VP, _VP, _VP]),
     "wg_ctx_set_profile": (_I, [_VP, _VP]),
     "wg_ctx_geometry": (_I, [_VP, _PI64, _PI64, _PI, _PI]),
     "wg_strerror": (ctypes.c_char_p, [_I]),

@@ -1887,6 +1887,47 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     }
 }
 
+// ---------------------------------------------------------------------------
+// replica diagnostics (optim.py:199-210): sum of replicas, spread potential
+// ---------------------------------------------------------------------------
+
+struct ReplicaPtrs {
+    const void* w[kMaxJobs];
+};
+
+// sum[e] += sum_r W_r[e] (fp64)
+template <typename T>
+__global__ void replicas_sum_kernel(ReplicaPtrs ptrs, int R, int64_t n, double* sum) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        for (int r = 0; r < R; ++r) acc += double(static_cast<const T*>(ptrs.w[r])[e]);
+        sum[e] += acc;
+    }
+}
+
+// out[0] += sum_r sum_e (W_r[e] - mu[e])^2 ; out[1] = max over r, e of |W_r[e] - W_0[e]|
+template <typename T>
+__global__ void replicas_spread_kernel(ReplicaPtrs ptrs, int R, int64_t n, const double* mu, double* out) {
+    double g = 0.0, dmax = 0.0;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        const double m = mu[e];
+        const double w0 = double(static_cast<const T*>(ptrs.w[0])[e]);
+        for (int r = 0; r < R; ++r) {
+            const double w = double(static_cast<const T*>(ptrs.w[r])[e]);
+            g += (w - m) * (w - m);
+            dmax = fmax(dmax, fabs(w - w0));
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        g += __shfl_xor_sync(0xffffffffu, g, o);
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&out[0], g);
+        atomicMax(reinterpret_cast<unsigned long long*>(&out[1]), __double_as_longlong(dmax));  // dmax >= 0
+    }
+}
+
 __global__ void fill_i64_kernel(int64_t* p, int64_t n, int64_t v) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) p[i] = v;
 }
@@ -2524,6 +2565,34 @@ int wg_delay(wg_ctx* ctx, int64_t ns, void* stream) {
     if (ns <= 0) return WG_OK;
     WG_CUDA(cudaSetDevice(ctx->cfg.device));
     delay_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(ns);
+    WG_CUDA(cudaGetLastError());
+    return WG_OK;
+}
+
+int wg_replicas_sum(wg_ctx* ctx, const void* const* W, int R, double* sum, void* stream) {
+    if (!ctx || !W || !sum || R < 1 || R > kMaxJobs) return fail(WG_EINVAL, "bad replica list");
+    ReplicaPtrs rp;
+    for (int r = 0; r < R; ++r) rp.w[r] = W[r];
+    WG_CUDA(cudaSetDevice(ctx->cfg.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (ctx->cfg.dtype == WG_F32)
+        replicas_sum_kernel<float><<<ctx->sms * 4, 256, 0, s>>>(rp, R, ctx->cfg.n, sum);
+    else
+        replicas_sum_kernel<double><<<ctx->sms * 4, 256, 0, s>>>(rp, R, ctx->cfg.n, sum);
+    WG_CUDA(cudaGetLastError());
+    return WG_OK;
+}
+
+int wg_replicas_spread(wg_ctx* ctx, const void* const* W, int R, const double* mu, double* out, void* stream) {
+    if (!ctx || !W || !mu || !out || R < 1 || R > kMaxJobs) return fail(WG_EINVAL, "bad replica list");
+    ReplicaPtrs rp;
+    for (int r = 0; r < R; ++r) rp.w[r] = W[r];
+    WG_CUDA(cudaSetDevice(ctx->cfg.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (ctx->cfg.dtype == WG_F32)
+        replicas_spread_kernel<float><<<ctx->sms * 4, 256, 0, s>>>(rp, R, ctx->cfg.n, mu, out);
+    else
+        replicas_spread_kernel<double><<<ctx->sms * 4, 256, 0, s>>>(rp, R, ctx->cfg.n, mu, out);
     WG_CUDA(cudaGetLastError());
     return WG_OK;
 }

@@ -1,0 +1,55 @@
+"""Replica diagnostics on the device (drop-in for the replica part of `wagma.optim.compute_diagnostics`).
+
+The reference's `compute_diagnostics` (optim.py:199-210) reports the replica
+mean mu_t and the spread potential Gamma_t = sum_r ||W_r - mu_t||^2, and its
+recorder asserts that replicas are bit-identical after every global sync
+(optim.py:289-293). Here the sums run in fp64 on the device
+(`wg_replicas_sum` / `wg_replicas_spread`); across processes the replica sum
+vector and the spread are all-reduced with torch.distributed. The problem
+terms (loss and gradient norm at mu) belong to the synthetic problems, which
+are out of scope.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Mapping, Optional
+
+import torch
+
+from .context import DeviceContext
+
+__all__ = ["ReplicaDiagnostics", "replica_diagnostics"]
+
+
+@dataclass
+class ReplicaDiagnostics:
+    mu: torch.Tensor          # fp64 replica mean over all P ranks
+    gamma: float              # sum_r ||W_r - mu||^2 over all P ranks
+    identical: bool           # every replica bit-identical (gamma == 0 exactly)
+
+
+def replica_diagnostics(ctx: DeviceContext, replicas: Mapping[int, torch.Tensor],
+                        process_group=None) -> ReplicaDiagnostics:
+    ranks = sorted(replicas)
+    if sorted(ranks) != list(ctx.local_ranks):
+        raise ValueError("pass the replicas of every rank this process hosts")
+    for r in ranks:
+        ctx._check_vec(replicas[r], f"W[{r}]")
+    ptrs = (ctypes.c_void_p * len(ranks))(*[replicas[r].data_ptr() for r in ranks])
+    stream = ctx.stream_handle()
+    total = torch.zeros(ctx.n, dtype=torch.float64, device=ctx.torch_device)
+    ctx._raise(ctx.lib.wg_replicas_sum(ctx._h, ptrs, len(ranks), total.data_ptr(), stream), "wg_replicas_sum")
+    import torch.distributed as dist
+    multi = ctx.n_gpus > 1 and dist.is_available() and dist.is_initialized()
+    if multi:
+        dist.all_reduce(total, group=process_group)
+    mu = total / ctx.P
+    out = torch.zeros(2, dtype=torch.float64, device=ctx.torch_device)
+    ctx._raise(ctx.lib.wg_replicas_spread(ctx._h, ptrs, len(ranks), mu.data_ptr(), out.data_ptr(), stream),
+               "wg_replicas_spread")
+    if multi:
+        dist.all_reduce(out[:1], group=process_group)
+    gamma = float(out[0].item())
+    return ReplicaDiagnostics(mu=mu, gamma=gamma, identical=gamma == 0.0)

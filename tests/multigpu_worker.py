@@ -69,7 +69,10 @@ def main():
     torch.cuda.synchronize()
     ctx.check()
     dist.barrier()
+    from paper_2005_00124_b200.diagnostics import replica_diagnostics
+    diag = replica_diagnostics(ctx, opt.W)
     out = {f"W{r}": opt.W[r].cpu().numpy() for r in ctx.local_ranks}
+    out["gamma"] = np.array(diag.gamma)
     for (t, r), v in grads.items():
         out[f"g{t}_{r}"] = v.cpu().numpy()
     out["w0"] = w0.cpu().numpy()

@@ -67,6 +67,10 @@ def test_multigpu_live_protocol_bit_exact(tmp_path, G, P, S, T, tau, n, dtype, v
                               stamps=stamps, alpha=bool(alpha), beta=not alpha, update_rule="momentum",
                               momentum=0.9, dtype=npdt)
     assert np.array_equal(W, want)
+    # device spread potential Gamma (all-reduced across the GPUs) vs numpy
+    W64 = W.astype(np.float64)
+    gamma = float(((W64 - W64.mean(axis=0)) ** 2).sum())
+    assert float(outs[0]["gamma"]) == pytest.approx(gamma, rel=1e-9)
     if alpha:
         for v in range(T):
             if (v + 1) % tau == 0:

@@ -205,3 +205,23 @@ def test_launch_validation(cuda):
     with pytest.raises(InvalidParamsError):  # wrong dtype / size
         ctx.launch([Job(0, _lib.WG_JOB_STEP, 0, W=torch.zeros(n + 1, device="cuda"), g=g)])
     ctx.close()
+
+
+def test_replica_diagnostics(cuda):
+    """Gamma_t and the post-sync bit-identity check (optim.py:199-210, 289-293)."""
+    from paper_2005_00124_b200.diagnostics import replica_diagnostics
+    P, S, n, tau, T = 4, 2, 3001, 3, 6
+    ctx = DeviceContext(P, S, n, tau=tau, timeout_s=5.0)
+    cfg = OptimizerConfig(T=T, S=S, tau=tau, eta=EtaSchedule(value=0.1), update_rule="momentum")
+    opt = GroupAveragingOptimizer(ctx, cfg, torch.randn(n, device="cuda"))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for t in range(T):
+        opt.step(t, {r: torch.randn(n, device="cuda", generator=g) for r in range(P)})
+        torch.cuda.synchronize()
+        d = replica_diagnostics(ctx, opt.W)
+        W = np.stack([opt.W[r].cpu().numpy().astype(np.float64) for r in range(P)])
+        mu = W.mean(axis=0)
+        assert np.allclose(d.mu.cpu().numpy(), mu, rtol=0, atol=1e-12)
+        assert d.gamma == pytest.approx(float(((W - mu) ** 2).sum()), rel=1e-9)
+        assert d.identical == ((t + 1) % tau == 0)  # bit-identical exactly after each global sync
+    ctx.close()
