@@ -1011,12 +1011,27 @@ constexpr int kNvlDepth = WG_NVL_DEPTH;  // producer cp.async ring depth (items)
 #define WG_SPLIT_NSB 16
 #endif
 constexpr int kSplitDepth = WG_SPLIT_DEPTH;  // producer ring depth in the split kernel
+// split kernel: 1 = leaves on this GPU are TMA-copied into the stage like
+// remote ones; 0 = reducers read them straight from L2 (they were produced
+// by this CTA moments ago), and the shared memory goes to the producers
+#ifndef WG_SPLIT_NSA_MIN  // stream-A stages reserved before stream B takes the rest
+#define WG_SPLIT_NSA_MIN 4
+#endif
+#ifndef WG_SPLIT_ABATCH  // stream-A tiles per flag-poll batch (0: NSA - 1)
+#define WG_SPLIT_ABATCH 0
+#endif
+#ifndef WG_SPLIT_TMA_LOCAL
+#define WG_SPLIT_TMA_LOCAL 1
+#endif
 constexpr int kNvlMaxStages = 16;
 constexpr int kNvlThreads = 2 * kThreads + 32;
 constexpr int kNvlMaxDyn = 200 * 1024;
 constexpr int kPollPerLane = 8;
 constexpr int kPullBatch = 8;  // tiles whose flags are polled and copies issued together
-constexpr int kPubChunk = 8;   // tiles published together (one fence per chunk)
+#ifndef WG_PUB_CHUNK
+#define WG_PUB_CHUNK 8
+#endif
+constexpr int kPubChunk = WG_PUB_CHUNK;  // tiles published together (one fence per chunk)
 constexpr int kPubRing = 16;   // per-chunk producer-completion counters (drift bound kPubRing/2 chunks)
 constexpr int kRedRing = 32;   // per-tile reducer counters (reducers drift < kNvlMaxStages tiles)
 constexpr int kMaxPoll = 32 * kPollPerLane;  // (leaf, warp) flags polled per tile
@@ -1414,6 +1429,12 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
 // ---------------------------------------------------------------------------
 
 constexpr int kSplitThreads = 22 * 32;
+// puller wait counters for tools/phase_profile.py (off: they cost registers)
+#ifdef WG_PROF_COUNTERS
+#define WG_PCNT(...) __VA_ARGS__
+#else
+#define WG_PCNT(...)
+#endif
 constexpr int kFinThreads = 4 * 32;
 
 // Owner of a tile of a split sum: rotates along each CTA's tile sequence so
@@ -1434,6 +1455,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     __shared__ int64_t metaA_tile[kNvlMaxStages], metaB_tile[kNvlMaxStages];
     __shared__ unsigned metaA_mask[kNvlMaxStages], metaB_mask[kNvlMaxStages];
     __shared__ int leaf_base[kMaxPlans + 1];
+    __shared__ int8_t row_of[kMaxPlans][kMaxLeaves];  // stage row of a leaf, -1: read from L2
+    __shared__ int plan_rows[kMaxPlans + 1];
     __shared__ volatile int ready;
     __shared__ int16_t poll_q[kMaxPoll];
     __shared__ int8_t poll_w[kMaxPoll];
@@ -1463,20 +1486,29 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             mbar_init(&fullB[st], 1);
             mbar_init(&emptyB[st], kFinThreads / 32);
         }
-        int acc = 0;
+        int acc = 0, rows = 0;
         for (int pl = 0; pl < NP; ++pl) {
             leaf_base[pl] = acc;
             acc += p.plans[pl].n_leaves;
+            int pr = 0;
+            for (int li = 0; li < p.plans[pl].n_leaves; ++li) {
+                const bool tma = WG_SPLIT_TMA_LOCAL || p.plans[pl].leaves[li] / p.R != p.gpu_index;
+                row_of[pl][li] = int8_t(tma ? rows++ : -1);
+                pr += tma;
+            }
+            plan_rows[pl] = pr;
         }
         leaf_base[NP] = acc;
+        plan_rows[NP] = rows;
     }
     if (tid < kMaxVersions) sm.activator[tid] = 0;
     if (tid < kPubRing) pub_count[tid] = 0;
     if (tid < kRedRing) red_count[tid] = 0;
     __syncthreads();
     const int NL = leaf_base[NP];
-    V* ringA = reinterpret_cast<V*>(dyn_smem);              // [NSA][NL][kThreads]
-    V* ringB = ringA + size_t(NSA) * NL * kThreads;           // [NSB][NP][kThreads]
+    const int NR = plan_rows[NP];  // stage rows: leaves copied by TMA
+    V* ringA = reinterpret_cast<V*>(dyn_smem);              // [NSA][NR][kThreads]
+    V* ringB = ringA + size_t(NSA) * NR * kThreads;           // [NSB][NP][kThreads]
     V* ring = ringB + size_t(NSB) * NP * kThreads;            // [kSplitDepth][3][kThreads]
     const int64_t my_ntiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const unsigned tile_bytes = unsigned(p.tile_elems * int64_t(sizeof(T)));
@@ -1500,7 +1532,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
 
     const long long t_start = clock64();
     auto prof_set = [&](int slot, long long v) {
-        if (p.prof) p.prof[blockIdx.x * 8 + slot] = v;
+        if (p.prof) p.prof[blockIdx.x * 16 + slot] = v;
     };
     if (warp < kWarps) {
         my_tiles = nvl_produce<T, kSplitDepth>(p, ring, my_ntiles, pub_count);
@@ -1547,15 +1579,21 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 plan_split[pl] = split && remote;
             }
             __threadfence_block();
+#ifdef WG_PROF_NOCONSUME  // profiling only: producers alone (results are garbage)
+            ready = 2;
+#else
             ready = aborted(p) ? 2 : 1;
+#endif
         } else if (!resolved && lane == 0) {
             ready = 2;
         }
         __syncwarp();
         resolved = resolved && ready == 1;
-        const int batch = NSA - 1 < kPullBatch ? (NSA > 1 ? NSA - 1 : 1) : kPullBatch;
+        int batch = NSA - 1 < kPullBatch ? (NSA > 1 ? NSA - 1 : 1) : kPullBatch;
+        if (WG_SPLIT_ABATCH > 0 && WG_SPLIT_ABATCH < batch) batch = WG_SPLIT_ABATCH;
         int64_t kA = 0, kc = 0;
         bool ok = resolved;
+        WG_PCNT(long long a_empty = 0, a_poll = 0, a_batches = 0;)
         while (ok) {
             // next batch of tiles with stream-A work
             if (lane == 0) {
@@ -1576,10 +1614,12 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             kc = __shfl_sync(0xffffffffu, kc, 0);
             const int nb = bt_n;
             if (nb == 0) break;
+            WG_PCNT(long long c0 = clock64();)
             for (int b = 0; b < nb && ok; ++b) {
                 const int64_t k = kA + b;
                 if (k >= NSA && !mbar_wait(p, &emptyA[k % NSA], unsigned((k / NSA - 1) & 1))) ok = false;
             }
+            WG_PCNT(a_empty += clock64() - c0; c0 = clock64(); ++a_batches;)
             if (!ok) {
                 if (lane == 0) raise_error(p, WG_ETIMEOUT, kA);
                 break;
@@ -1631,13 +1671,14 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 }
             }
             if (__any_sync(0xffffffffu, rc != 0)) break;
+            WG_PCNT(a_poll += clock64() - c0;)
             acquire_for_tma();
             if (lane == 0) {
                 for (int b = 0; b < nb; ++b) {
                     const int st = int((kA + b) % NSA);
                     unsigned rows = 0;
                     for (int pl = 0; pl < NP; ++pl)
-                        if (bt_mask[b] >> pl & 1) rows += p.plans[pl].n_leaves;
+                        if (bt_mask[b] >> pl & 1) rows += plan_rows[pl];
                     metaA_tile[st] = bt_tile[b];
                     metaA_mask[st] = bt_mask[b];
                     mbar_arrive_expect_tx(&fullA[st], rows * tile_bytes);
@@ -1650,10 +1691,12 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 while (leaf_base[pl + 1] <= f) ++pl;
                 if (!(bt_mask[b] >> pl & 1)) continue;
                 const int li = f - leaf_base[pl];
+                const int r = row_of[pl][li];
+                if (r < 0) continue;
                 const int st = int((kA + b) % NSA);
                 const T* src =
                     ring_ptr<T>(p, p.plans[pl].leaves[li], sm.leaf_slot[pl][li]) + bt_tile[b] * p.tile_elems;
-                bulk_g2s(ringA + (size_t(st) * NL + f) * kThreads, src, tile_bytes, &fullA[st]);
+                bulk_g2s(ringA + (size_t(st) * NR + r) * kThreads, src, tile_bytes, &fullA[st]);
             }
             __syncwarp();
             kA += nb;
@@ -1664,6 +1707,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             metaA_tile[kA % NSA] = -1;
             mbar_arrive(&fullA[kA % NSA]);
             prof_set(1, clock64() - t_start);
+            WG_PCNT(prof_set(8, a_empty); prof_set(9, a_poll); prof_set(10, a_batches);)
         }
     } else if (warp <= 2 * kWarps) {
         // ---------------- stream A reducers ----------------
@@ -1682,13 +1726,20 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             if (tile < 0) break;
             const unsigned mask = metaA_mask[st];
             const int64_t idx = tile * p.tile_elems + int64_t(ctid) * E;
-            const V* lb = ringA + size_t(st) * NL * kThreads;
+            const V* lb = ringA + size_t(st) * NR * kThreads;
             bool owned = false;
             for (int pl = 0; pl < NP; ++pl) {
                 if (!(mask >> pl & 1)) continue;
                 const DevPlan& P_ = p.plans[pl];
+                // local leaves from L2 (.cg: never a stale L1 line of a reused slot)
                 const int base = leaf_base[pl];
-                auto fetch = [&](int leaf) -> V { return lb[(base + leaf) * kThreads + ctid]; };
+                auto fetch = [&](int leaf) -> V {
+                    if (WG_SPLIT_TMA_LOCAL) return lb[(base + leaf) * kThreads + ctid];  // row == leaf index
+                    const int r = row_of[pl][leaf];
+                    if (r >= 0) return lb[r * kThreads + ctid];
+                    return __ldcg(reinterpret_cast<const V*>(
+                        ring_ptr<T>(p, P_.leaves[leaf], sm.leaf_slot[pl][leaf]) + idx));
+                };
                 const V acc = tree_sum<T>(fetch, P_.log_leaves);
                 if (plan_split[pl]) {  // this GPU owns the tile: publish the reduced tile
                     __stcg(reinterpret_cast<V*>(red_ptr<T>(p, split_owner(p, pl, tile),
@@ -1741,6 +1792,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         while (ready == 0) __nanosleep(64);
         int64_t kB = 0, kc = 0;
         bool ok = ready == 1;
+        WG_PCNT(long long b_empty = 0, b_poll = 0, b_notready = 0;)
         int batch = NSB - 1 < kPullBatch ? (NSB > 1 ? NSB - 1 : 1) : kPullBatch;
         batch = batch * NP > 32 ? (32 / NP > 0 ? 32 / NP : 1) : batch;  // one flag per lane
         while (ok) {
@@ -1775,14 +1827,17 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             int rc = 0;
             // usual case: every owner already published -> one fence for the batch
             const bool all_ready = __all_sync(0xffffffffu, !fp || x >= want);
+            WG_PCNT(b_notready += !all_ready;)
             if (all_ready) acquire_for_tma();
             for (int bb = 0; bb < nb && ok; ++bb) {
                 const int64_t k = kB + bb;
                 const int st = int(k % NSB);
+                WG_PCNT(long long c0 = clock64();)
                 if (k >= NSB && !mbar_wait(p, &emptyB[st], unsigned((k / NSB - 1) & 1))) {
                     ok = false;
                     break;
                 }
+                WG_PCNT(b_empty += clock64() - c0; c0 = clock64();)
                 if (!all_ready && fp && e / NP == bb) {
                     const uint64_t t0 = globaltimer();
                     int it = 0;
@@ -1801,6 +1856,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                     ok = false;
                     break;
                 }
+                WG_PCNT(b_poll += clock64() - c0;)
                 if (!all_ready) acquire_for_tma();
                 const int64_t tile = btB_tile[bb];
                 const unsigned mb = btB_mask[bb];
@@ -1829,6 +1885,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             metaB_tile[kB % NSB] = -1;
             mbar_arrive(&fullB[kB % NSB]);
             prof_set(5, clock64() - t_start);
+            WG_PCNT(prof_set(11, b_empty); prof_set(12, b_poll); prof_set(13, b_notready);)
         }
     } else {
         // ---------------- stream B finishers (2 vectors per thread) ----------------
@@ -2460,11 +2517,17 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         // reduced tiles their peers wait for
         // stream B (1 row per plan) gets what stream A (all leaves) leaves
         // after 4 stages, between 2 and 16 stages each
-        const size_t rowsA = size_t(std::max(n_leaves_total, 1)) * row, rowsB = size_t(p.n_plans) * row;
+        int n_rows_split = 0;
+        for (int k = 0; k < p.n_plans; ++k)
+            for (int li = 0; li < p.plans[k].n_leaves; ++li)
+                n_rows_split += WG_SPLIT_TMA_LOCAL || p.plans[k].leaves[li] / ctx->R != c.gpu_index;
+        const size_t rowsA = size_t(std::max(n_rows_split, 1)) * row, rowsB = size_t(p.n_plans) * row;
         const size_t split_fixed = size_t(kSplitDepth * 3) * row;
         const size_t avail = size_t(kNvlMaxDyn) > split_fixed ? size_t(kNvlMaxDyn) - split_fixed : 0;
         const int nsb = int(std::max<size_t>(
-            2, std::min<size_t>(WG_SPLIT_NSB, avail > 4 * rowsA ? (avail - 4 * rowsA) / rowsB : 0)));
+            2, std::min<size_t>(WG_SPLIT_NSB, avail > WG_SPLIT_NSA_MIN * rowsA
+                                                  ? (avail - WG_SPLIT_NSA_MIN * rowsA) / rowsB
+                                                  : 0)));
         const size_t fixed = split_fixed + size_t(nsb) * rowsB;
         const int nsa = fixed >= size_t(kNvlMaxDyn)
                             ? 0
@@ -2473,7 +2536,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
             return fail(WG_EINVAL, "split launch does not fit shared memory (%d leaves)", n_leaves_total);
         p.nvl_stages = nsa;
         p.split_stages = nsb;
-        const size_t smem_split = fixed + size_t(nsa) * n_leaves_total * row;
+        const size_t smem_split = fixed + size_t(nsa) * n_rows_split * row;
         const int di = c.dtype == WG_F32 ? 0 : 1;
         if (ctx->occ_split[di] <= 0) {
             int o = 0;

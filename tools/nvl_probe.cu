@@ -82,6 +82,121 @@ __global__ void tma_kernel(const char* src, size_t bytes, float* out) {
     if (acc == 1234.5f) out[0] = acc;
 }
 
+// all-to-all: chunk c comes from source c % nsrc (every peer read concurrently)
+struct Srcs { const char* p[8]; };
+__global__ void tma_multi_kernel(Srcs srcs, int nsrc, size_t bytes_per_src, float* out) {
+    extern __shared__ __align__(128) char smem[];
+    __shared__ uint64_t bars[kStages];
+    const size_t per = bytes_per_src / kChunk, nchunks = per * nsrc;
+    if (threadIdx.x == 0)
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    auto src_of = [&](size_t c) { return srcs.p[c % nsrc] + (c / nsrc) * kChunk; };
+    if (threadIdx.x == 0)
+        for (int s = 0; s < kStages; ++s) {
+            size_t c = blockIdx.x + size_t(s) * gridDim.x;
+            if (c < nchunks) {
+                mbar_expect_tx(&bars[s], kChunk);
+                bulk_g2s(smem + s * kChunk, src_of(c), kChunk, &bars[s]);
+            }
+        }
+    float acc = 0.f;
+    int it = 0;
+    for (size_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+        const int s = it % kStages;
+        mbar_wait(&bars[s], (it / kStages) & 1);
+        const float4* v = reinterpret_cast<const float4*>(smem + s * kChunk);
+        for (int i = threadIdx.x; i < kChunk / 16; i += blockDim.x) {
+            float4 x = v[i];
+            acc += x.x + x.y + x.z + x.w;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            size_t cn = c + size_t(kStages) * gridDim.x;
+            if (cn < nchunks) {
+                mbar_expect_tx(&bars[s], kChunk);
+                bulk_g2s(smem + s * kChunk, src_of(cn), kChunk, &bars[s]);
+            }
+        }
+    }
+    if (acc == 1234.5f) out[0] = acc;
+}
+
+// HBM streaming copy, to load the memory system while the pulls run
+__global__ void hbm_copy_kernel(const float4* a, float4* b, size_t n16) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n16; i += size_t(gridDim.x) * blockDim.x)
+        b[i] = __ldcs(a + i);
+}
+
+static int all_to_all(int n, size_t bytes, bool with_hbm) {
+    // every GPU pulls `bytes` from each of its n-1 peers at the same time
+    char* buf[8];
+    float* out[8];
+    float4 *ha[8], *hb[8];
+    const size_t hbm_bytes = size_t(2) << 30;
+    for (int g = 0; g < n; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaMalloc(&buf[g], bytes));
+        CK(cudaMemset(buf[g], 0, bytes));
+        CK(cudaMalloc(&out[g], 4));
+        CK(cudaMalloc(&ha[g], hbm_bytes));
+        CK(cudaMalloc(&hb[g], hbm_bytes));
+        for (int q = 0; q < n; ++q)
+            if (q != g) {
+                cudaError_t pe = cudaDeviceEnablePeerAccess(q, 0);
+                if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) CK(pe);
+                cudaGetLastError();
+            }
+        CK(cudaFuncSetAttribute(tma_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * kChunk));
+    }
+    int sms;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    cudaEvent_t a[8], b[8], c[8], d[8];
+    cudaStream_t s1[8], s2[8];
+    for (int g = 0; g < n; ++g) {
+        CK(cudaSetDevice(g));
+        cudaEventCreate(&a[g]); cudaEventCreate(&b[g]); cudaEventCreate(&c[g]); cudaEventCreate(&d[g]);
+        cudaStreamCreateWithFlags(&s1[g], cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&s2[g], cudaStreamNonBlocking);
+    }
+    for (int rep = 0; rep < 3; ++rep) {
+        for (int g = 0; g < n; ++g) {
+            CK(cudaSetDevice(g));
+            Srcs srcs;
+            int k = 0;
+            for (int q = 0; q < n; ++q)
+                if (q != g) srcs.p[k++] = buf[q];
+            const int pull_ctas = with_hbm ? sms / 2 : sms;
+            cudaEventRecord(a[g], s1[g]);
+            tma_multi_kernel<<<pull_ctas, 128, kStages * kChunk, s1[g]>>>(srcs, n - 1, bytes, out[g]);
+            cudaEventRecord(b[g], s1[g]);
+            if (with_hbm) {
+                cudaEventRecord(c[g], s2[g]);
+                hbm_copy_kernel<<<sms * 4, 256, 0, s2[g]>>>(ha[g], hb[g], hbm_bytes / 16);
+                cudaEventRecord(d[g], s2[g]);
+            }
+        }
+        for (int g = 0; g < n; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaDeviceSynchronize());
+            CK(cudaGetLastError());
+            float ms, ms2 = 0.f;
+            cudaEventElapsedTime(&ms, a[g], b[g]);
+            if (with_hbm) cudaEventElapsedTime(&ms2, c[g], d[g]);
+            if (rep == 2)
+                printf("a2a n=%d gpu %d: pull %.3f ms %.1f GB/s ingress%s", n, g, ms, bytes * (n - 1) / ms / 1e6,
+                       with_hbm ? "" : "\n");
+            if (rep == 2 && with_hbm) printf("  | hbm copy %.3f ms %.1f GB/s\n", ms2, 2.0 * hbm_bytes / ms2 / 1e6);
+        }
+    }
+    for (int g = 0; g < n; ++g) {
+        CK(cudaSetDevice(g));
+        cudaFree(buf[g]); cudaFree(out[g]); cudaFree(ha[g]); cudaFree(hb[g]);
+    }
+    return 0;
+}
+
 __global__ void cpasync_kernel(const float4* src, size_t n16, float* out) {
     extern __shared__ __align__(16) float4 ring[];  // [4][blockDim]
     float acc = 0.f;
@@ -115,6 +230,13 @@ int main(int argc, char** argv) {
     size_t bytes = argc > 1 ? strtoull(argv[1], nullptr, 10) : (size_t(1) << 30);
     int n;
     CK(cudaGetDeviceCount(&n));
+    if (argc > 2 && argv[2][0] == 'a') {  // tools/nvl_probe BYTES a2a: all-to-all pulls
+        for (int k = 2; k <= n; k *= 2) {
+            if (all_to_all(k, bytes / 4, false)) return 1;
+            if (all_to_all(k, bytes / 4, true)) return 1;
+        }
+        return 0;
+    }
     int peer = n > 1 ? 1 : 0;
     char* buf;
     CK(cudaSetDevice(peer));

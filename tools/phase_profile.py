@@ -34,7 +34,7 @@ ctx = DeviceContext(a.P, a.S, a.nelem, tau=a.tau, n_gpus=G, gpu_index=rank, devi
 opt = GroupAveragingOptimizer(ctx, OptimizerConfig(T=1 << 30, S=a.S, tau=a.tau, eta=EtaSchedule(value=0.1),
                                                    update_rule="momentum"), torch.zeros(a.nelem, device=dev))
 g = {r: torch.randn(a.nelem, device=dev) * 0.01 for r in ctx.local_ranks}
-prof = torch.zeros(ctx.grid * 8, dtype=torch.int64, device=dev)
+prof = torch.zeros(ctx.grid * 16, dtype=torch.int64, device=dev)
 ctx.lib.wg_ctx_set_profile(ctx._h, ctypes.c_void_p(prof.data_ptr()))
 ghz = 1.965
 for t in range(a.iters):
@@ -48,15 +48,18 @@ for t in range(a.iters):
     torch.cuda.synchronize()
     t = t * 8 + 7
     if True:
-        p = prof.view(-1, 8).cpu().numpy().astype(np.float64)
+        split_prof = os.environ.get("WG_PROF_SPLIT", "0") == "1"
+        p = prof.view(-1, 16 if split_prof else 8).cpu().numpy().astype(np.float64)
         if os.environ.get("WG_PROF_SPLIT", "0") == "1":
-            names = ["producer_total", "pullA_total", "x", "redA_full_wait", "redA_total", "pullB_total", "finB_full_wait", "finB_total"]
+            names = ["producer_total", "pullA_total", "x", "redA_full_wait", "redA_total", "pullB_total", "finB_full_wait", "finB_total", "pullA_empty", "pullA_poll", "x", "pullB_empty", "pullB_poll", "x", "x", "x"]
         elif os.environ.get("WG_NVL", "1") != "0":
             names = ["producer_total", "pull_empty_wait", "pull_poll", "pull_issue", "cons_full_wait", "x", "cons_total", "cons_ready_wait"]
         else:
             names = ["produce", "publish", "resolve", "poll", "consume", "tiles", "fence"]
         us = {nm: p[:, i].mean() / ghz / 1000 for i, nm in enumerate(names) if nm not in ("tiles", "x")}
         sync = (t + 1) % a.tau == 0
+        if os.environ.get("WG_PROF_DUMP"):
+            np.save(f"{os.environ['WG_PROF_DUMP']}_r{rank}_t{t}.npy", p)
         mx = {nm: p[:, i].max() / ghz / 1000 for i, nm in enumerate(names) if nm not in ("tiles", "x")}
         print(f"rank{rank} t={t} {'sync ' if sync else 'group'} kernel={ev0.elapsed_time(ev1)*1000:.0f}us "
               + " ".join(f"{k}={v:.0f}/{mx[k]:.0f}" for k, v in us.items()), flush=True)
