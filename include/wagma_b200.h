@@ -154,9 +154,12 @@ typedef struct {
     int64_t version;
     int64_t contrib_stamp; /* stamp this rank contributed (collective.py:289)  */
     int32_t timely;        /* stamp == version (collective.py:301)             */
-    int32_t activator;     /* this launch raised the activation flag           */
+    int32_t activator;     /* this rank raised the activation flag (is root)    */
     int32_t error;         /* WG_* device-side error latched for this job      */
-    int32_t pad;
+    int32_t root;          /* rank that raised the version's activation flag,
+                              -1 if none (sync, blocking or replayed versions);
+                              the root of the reference's binomial ACT tree
+                              (collective.py:263-274)                          */
 } wg_job_status;
 
 /* One launch = at most one job per local rank. forced_stamps (may be NULL)

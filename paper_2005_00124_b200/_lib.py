@@ -46,7 +46,7 @@ class WgJobStatus(ctypes.Structure):
     _fields_ = [
         ("version", ctypes.c_int64), ("contrib_stamp", ctypes.c_int64),
         ("timely", ctypes.c_int32), ("activator", ctypes.c_int32),
-        ("error", ctypes.c_int32), ("pad", ctypes.c_int32),
+        ("error", ctypes.c_int32), ("root", ctypes.c_int32),
     ]
 
 

@@ -187,9 +187,29 @@ class GroupAllreduce:
         self.completion_tag = -1
         self.execution_count: dict[int, int] = {}
         self.activations_originated = 0
+        # message-count equivalents of the reference's simulated transport
+        # (collective.py:182-184): ACTs of the binomial activation tree rooted
+        # at the activating rank, one PHASE message per butterfly phase
+        self.acts_sent = 0
+        self.phases_sent = 0
+        self._tree_depth = P.bit_length() - 1
+        self._group_phases = S.bit_length() - 1
 
     def install_fresh(self, vec, iteration: int) -> None:
         self.send_buffer.install(vec, iteration)
+
+    def _acts_for(self, root: int) -> int:
+        # the root sends on every tree edge j < log2 P (collective.py:263-268);
+        # rank root ^ q receives at hop msb(q) and forwards on j > hop (:270-274)
+        if root < 0:
+            return 0
+        q = self.rank ^ root
+        return self._tree_depth if q == 0 else self._tree_depth - q.bit_length()
+
+    def handle_message(self, src: int, body: bytes) -> None:
+        """The reference's transport hook (collective.py:226-233). Device memory
+        is the transport here: peers never exchange host messages."""
+        raise ProtocolFault(f"rank {self.rank}: no host messages on the device transport (from {src})")
 
     def join_or_check(self, version: int, fresh) -> JoinResult:
         """Join version ``version`` with the fresh local model (collective.py:192-222)."""
@@ -209,6 +229,8 @@ class GroupAllreduce:
             self.execution_count[version] = self.execution_count.get(version, 0) + 1
             if st.activator:
                 self.activations_originated += 1
+            self.acts_sent += self._acts_for(st.root)
+            self.phases_sent += self._group_phases
             if self.contribution_log is not None:
                 self.contribution_log.append((self.rank, version, st.contrib_stamp))
             self.last_completed = max(self.last_completed, version)

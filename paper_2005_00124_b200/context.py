@@ -68,6 +68,7 @@ class JobStatus:
     timely: bool
     activator: bool
     error: int
+    root: int = -1  # rank that raised the version's activation flag (-1: none)
 
 
 def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
@@ -273,7 +274,7 @@ class DeviceContext:
         for i in range(self._n_last):
             self._raise(self.lib.wg_launch_status(self._h, i, ctypes.byref(self._status)), "wg_launch_status")
             s = self._status
-            out.append(JobStatus(s.version, s.contrib_stamp, bool(s.timely), bool(s.activator), s.error))
+            out.append(JobStatus(s.version, s.contrib_stamp, bool(s.timely), bool(s.activator), s.error, s.root))
         return out
 
     def query_version(self, version: int) -> tuple[list[int], bool]:

@@ -72,7 +72,8 @@ static int fail(int code, const char* fmt, ...) {
 
 struct Desc {                 // activation descriptor of one group version
     int64_t state;            // 0 free; (v+1)*4+1 locking; (v+1)*4+2 locked
-    int64_t pad[15];
+    int64_t root;             // rank that raised the activation flag
+    int64_t pad[14];
     int64_t stamps[kMaxP];    // contribution stamp of every rank
 };
 
@@ -389,7 +390,14 @@ __device__ void control_phase(const LaunchParams& p, int* s_activator) {
         }
         act = __shfl_sync(0xffffffffu, act, 0);
         if (!act) continue;
-        if (lane == 0) s_activator[vi] = 1;
+        // the activation root: the lowest rank of this launch joining v
+        int root = p.P;
+        for (int j = 0; j < p.n_jobs; ++j)
+            if (p.jobs[j].vidx == vi && p.jobs[j].rank < root) root = p.jobs[j].rank;
+        if (lane == 0) {
+            s_activator[vi] = 1;
+            d->root = root;
+        }
         // Bounded grace window: ranks on other GPUs that join within it are
         // timely. Ranks on this GPU announced at launch start (final).
         const uint64_t t0 = globaltimer();
@@ -429,6 +437,13 @@ __device__ void control_phase(const LaunchParams& p, int* s_activator) {
         }
         __syncwarp();
     }
+}
+
+// Rank whose arrival raised the activation flag of a job's live group
+// version (read after the descriptor is locked), -1 for none.
+__device__ __forceinline__ int32_t activation_root(const LaunchParams& p, const DevJob& jb, bool resolved) {
+    if (!resolved || jb.vidx < 0 || p.versions[jb.vidx].mode != kLive) return -1;
+    return int32_t(ld_relaxed_sys(&desc_ptr(p, p.versions[jb.vidx].version)->root));
 }
 
 // ---------------------------------------------------------------------------
@@ -973,9 +988,9 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
             st.version = jb.version;
             st.contrib_stamp = (jb.kind == WG_JOB_LOCAL_STEP || !resolved) ? jb.version : sm.stamps[jb.vidx][jb.rank];
             st.timely = st.contrib_stamp == jb.version;
-            st.activator = jb.vidx >= 0 ? sm.activator[jb.vidx] : 0;
+            st.root = activation_root(p, jb, resolved);
+            st.activator = jb.vidx >= 0 && sm.activator[jb.vidx] && st.root == jb.rank;
             st.error = int32_t(ld_relaxed_sys(err_ptr(p)));
-            st.pad = 0;
             p.status[threadIdx.x] = st;
         }
     }
@@ -1402,9 +1417,9 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
             stt.version = jb.version;
             stt.contrib_stamp = (jb.kind == WG_JOB_LOCAL_STEP || !res) ? jb.version : sm.stamps[jb.vidx][jb.rank];
             stt.timely = stt.contrib_stamp == jb.version;
-            stt.activator = jb.vidx >= 0 ? sm.activator[jb.vidx] : 0;
+            stt.root = activation_root(p, jb, res);
+            stt.activator = jb.vidx >= 0 && sm.activator[jb.vidx] && stt.root == jb.rank;
             stt.error = int32_t(ld_relaxed_sys(err_ptr(p)));
-            stt.pad = 0;
             p.status[tid] = stt;
         }
     }
@@ -1936,9 +1951,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             stt.version = jb.version;
             stt.contrib_stamp = (jb.kind == WG_JOB_LOCAL_STEP || !res) ? jb.version : sm.stamps[jb.vidx][jb.rank];
             stt.timely = stt.contrib_stamp == jb.version;
-            stt.activator = jb.vidx >= 0 ? sm.activator[jb.vidx] : 0;
+            stt.root = activation_root(p, jb, res);
+            stt.activator = jb.vidx >= 0 && sm.activator[jb.vidx] && stt.root == jb.rank;
             stt.error = int32_t(ld_relaxed_sys(err_ptr(p)));
-            stt.pad = 0;
             p.status[tid] = stt;
         }
     }

@@ -166,3 +166,30 @@ def test_install_regression_rejected(cuda):
     with pytest.raises(ProtocolFault):
         node.group.install_fresh(np.ones(2), 3)
     ctx.close()
+
+
+def test_activation_tree_message_counts(cuda):
+    """Exactly one activator per version; the binomial ACT tree rooted at it
+    has P-1 edges and every member sends log2 S phase messages
+    (test_collective.py:231-245, collective.py:263-274, :319)."""
+    P, S, n_versions = 8, 4, 5
+    ctx = DeviceContext(P, S, 64, dtype=torch.float64, timeout_s=5.0)
+    nodes = [Node(ctx, r, P, S, np.zeros(64)) for r in range(P)]
+    rng = np.random.default_rng(3)
+    for v in range(n_versions):
+        late = {int(x) for x in rng.choice(P, 2, replace=False)} if v % 2 else set()
+        with ctx.batch():
+            for r in range(P):
+                if r not in late:
+                    nodes[r].group.join_or_check(v, rng.standard_normal(64))
+        if late:
+            with ctx.batch():
+                for r in sorted(late):
+                    nodes[r].group.join_or_check(v, rng.standard_normal(64))
+    groups = [nd.group for nd in nodes]
+    assert sum(g.activations_originated for g in groups) == n_versions
+    assert sum(g.acts_sent for g in groups) == (P - 1) * n_versions
+    assert all(g.phases_sent == 2 * n_versions for g in groups)
+    with pytest.raises(ProtocolFault):
+        groups[0].handle_message(1, b"")
+    ctx.close()

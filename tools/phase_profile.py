@@ -39,6 +39,8 @@ ctx.lib.wg_ctx_set_profile(ctx._h, ctypes.c_void_p(prof.data_ptr()))
 ghz = 1.965
 for t in range(a.iters):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()  # start the 8 launches together (skew > grace window makes a GPU stale)
     for u in range(8):  # back to back (steady state), profile the last launch
         if u == 7:
             prof.zero_()
@@ -61,7 +63,9 @@ for t in range(a.iters):
         if os.environ.get("WG_PROF_DUMP"):
             np.save(f"{os.environ['WG_PROF_DUMP']}_r{rank}_t{t}.npy", p)
         mx = {nm: p[:, i].max() / ghz / 1000 for i, nm in enumerate(names) if nm not in ("tiles", "x")}
-        print(f"rank{rank} t={t} {'sync ' if sync else 'group'} kernel={ev0.elapsed_time(ev1)*1000:.0f}us "
+        stamps, locked = ctx.query_version(t) if not sync else ([t] * a.P, True)
+        stale = sum(1 for x in stamps if x != t)
+        print(f"rank{rank} t={t} stale={stale} {'sync ' if sync else 'group'} kernel={ev0.elapsed_time(ev1)*1000:.0f}us "
               + " ".join(f"{k}={v:.0f}/{mx[k]:.0f}" for k, v in us.items()), flush=True)
 ctx.lib.wg_ctx_set_profile(ctx._h, None)
 ctx.check()
