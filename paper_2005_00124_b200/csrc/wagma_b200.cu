@@ -551,6 +551,14 @@ __device__ bool resolve_sources(const LaunchParams& p, SmemCtl& sm) {
 #define WG_DEPTH 3
 #endif
 constexpr int kDepth = WG_DEPTH;
+// single-GPU loop A/B knobs: incremental issue cursor; per-job ring slot
+// pointers from shared memory (else recomputed per item)
+#ifndef WG_STEP_INCR
+#define WG_STEP_INCR 0
+#endif
+#ifndef WG_STEP_SRING
+#define WG_STEP_SRING 0
+#endif
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int bytes) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
@@ -582,11 +590,22 @@ __device__ __forceinline__ void issue_item(const LaunchParams& p, int64_t tile, 
         cp_async16(&slot[2 * kThreads + tid], static_cast<const T*>(jb.m) + off, bytes);
 }
 
+// Send-ring slot of every job of the launch (the W' it installs), computed
+// once per CTA instead of a 64-bit modulo per item. Caller syncs after.
+template <typename T>
+__device__ __forceinline__ void init_ring_slots(const LaunchParams& p, T** ring_slot) {
+    if (threadIdx.x < p.n_jobs) {
+        const DevJob& jb = p.jobs[threadIdx.x];
+        ring_slot[threadIdx.x] = ring_ptr<T>(p, jb.rank, slot_of(p, jb.version));
+    }
+}
+
 // Local step of one item + send-ring install + stage (optim.py:176-183,
 // collective.py:95-101).
 template <typename T, bool STAGE = true>
 __device__ __forceinline__ void compute_item(const LaunchParams& p, int64_t tile, int j,
-                                             const typename Tr<T>::V* slot, typename Tr<T>::V* stage) {
+                                             const typename Tr<T>::V* slot, typename Tr<T>::V* stage,
+                                             T* const* ring_slot) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
     const int tid = threadIdx.x;
@@ -613,7 +632,8 @@ __device__ __forceinline__ void compute_item(const LaunchParams& p, int64_t tile
         }
     }
     // SendBuffer.install: W' written once into the send ring, and staged
-    __stcg(reinterpret_cast<V*>(ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + idx), wp);
+    T* const rs = ring_slot ? ring_slot[j] : ring_ptr<T>(p, jb.rank, slot_of(p, jb.version));
+    __stcg(reinterpret_cast<V*>(rs + idx), wp);
     if (STAGE) stage[j * kThreads + tid] = wp;
 }
 
@@ -647,7 +667,8 @@ __device__ __forceinline__ void load_job(const LaunchParams& p, const DevJob& jb
 }
 
 template <typename T>
-__device__ __forceinline__ void produce_tile_regs(const LaunchParams& p, int64_t tile, typename Tr<T>::V* stage) {
+__device__ __forceinline__ void produce_tile_regs(const LaunchParams& p, int64_t tile, typename Tr<T>::V* stage,
+                                                  T* const* ring_slot) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
     constexpr int U = kVecPerThread;
@@ -690,7 +711,7 @@ __device__ __forceinline__ void produce_tile_regs(const LaunchParams& p, int64_t
         }
         if (jb.produces) {
             // SendBuffer.install (collective.py:95-101): one write into the ring
-            T* slot = ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + tbase;
+            T* slot = ring_slot[j] + tbase;
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 __stcg(reinterpret_cast<V*>(slot + int64_t(k * kThreads + tid) * E), wp[k]);
@@ -890,8 +911,10 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     V* stage = reinterpret_cast<V*>(dyn_smem);
     __shared__ SmemCtl sm;
+    __shared__ T* s_ring[kMaxJobs];
     if (threadIdx.x == 0) sm.abort = 0;
     if (threadIdx.x < kMaxVersions) sm.activator[threadIdx.x] = 0;
+    init_ring_slots<T>(p, s_ring);
     __syncthreads();
     if (blockIdx.x == 0) {
         if (threadIdx.x < 32) control_phase(p, sm.activator);
@@ -914,7 +937,7 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
         int64_t tile = blockIdx.x;
         int buf = 0;
         if (tile < p.n_tiles) {
-            produce_tile_regs<T>(p, tile, stages[0]);
+            produce_tile_regs<T>(p, tile, stages[0], s_ring);
             lap(0);
             publish_tile(p, tile);
             lap(1);
@@ -923,7 +946,7 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
         while (tile < p.n_tiles) {
             const int64_t next = tile + gridDim.x;
             if (next < p.n_tiles) {
-                produce_tile_regs<T>(p, next, stages[buf ^ 1]);
+                produce_tile_regs<T>(p, next, stages[buf ^ 1], s_ring);
                 lap(0);
                 publish_tile(p, next);
                 lap(1);
@@ -950,6 +973,30 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
         V* ring = stage;  // [kDepth][3][kThreads], then the W' stage [J][kThreads]
         V* st = ring + kDepth * 3 * kThreads;
         const int64_t my_ntiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+#if WG_STEP_INCR
+        // issue cursor (tile ik of this CTA, job ij) runs kDepth items ahead;
+        // advanced incrementally (no 64-bit division per item)
+        int64_t ik = 0;
+        int ij = 0;
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) {
+            if (ik < my_ntiles) issue_item<T>(p, int64_t(blockIdx.x) + ik * gridDim.x, ij, ring + d * 3 * kThreads);
+            cp_async_commit();
+            if (++ij == J) ij = 0, ++ik;
+        }
+        int rs = 0;
+        for (int64_t kk = 0; kk < my_ntiles; ++kk) {
+            const int64_t tile = int64_t(blockIdx.x) + kk * gridDim.x;
+            for (int j = 0; j < J; ++j) {
+                cp_async_wait<kDepth - 1>();
+                V* slot = ring + rs * 3 * kThreads;
+                compute_item<T>(p, tile, j, slot, st, WG_STEP_SRING ? s_ring : nullptr);
+                if (ik < my_ntiles) issue_item<T>(p, int64_t(blockIdx.x) + ik * gridDim.x, ij, slot);
+                cp_async_commit();
+                if (++ij == J) ij = 0, ++ik;
+                if (++rs == kDepth) rs = 0;
+            }
+#else
         const int64_t n_items = my_ntiles * J;
 #pragma unroll
         for (int d = 0; d < kDepth; ++d) {
@@ -963,12 +1010,13 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
             for (int j = 0; j < J; ++j, ++i) {
                 cp_async_wait<kDepth - 1>();
                 V* slot = ring + (i % kDepth) * 3 * kThreads;
-                compute_item<T>(p, tile, j, slot, st);
+                compute_item<T>(p, tile, j, slot, st, WG_STEP_SRING ? s_ring : nullptr);
                 const int64_t nx = i + kDepth;
                 if (nx < n_items)
                     issue_item<T>(p, int64_t(blockIdx.x) + (nx / J) * int64_t(gridDim.x), int(nx % J), slot);
                 cp_async_commit();
             }
+#endif
             ++my_tiles;
             if (!resolved) {
                 if (!resolve_sources<T>(p, sm)) break;
@@ -1103,29 +1151,31 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // stores acquired through the shared-memory counter). Never waits on a peer.
 template <typename T, int kNvlDepth>
 __device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename Tr<T>::V* ring, int64_t my_ntiles,
-                                                unsigned* pub_count) {
+                                                unsigned* pub_count, T* const* ring_slot) {
     using V = typename Tr<T>::V;
     const int lane = threadIdx.x & 31;
     const int J = p.n_jobs;
     unsigned my_tiles = 0;
-    const int64_t n_items = my_ntiles * J;
+    // issue cursor kNvlDepth items ahead, advanced incrementally
+    int64_t ik = 0;
+    int ij = 0;
 #pragma unroll
     for (int d = 0; d < kNvlDepth; ++d) {
-        if (d < n_items)
-            issue_item<T>(p, int64_t(blockIdx.x) + (d / J) * int64_t(gridDim.x), d % J, ring + d * 3 * kThreads);
+        if (ik < my_ntiles) issue_item<T>(p, int64_t(blockIdx.x) + ik * gridDim.x, ij, ring + d * 3 * kThreads);
         cp_async_commit();
+        if (++ij == J) ij = 0, ++ik;
     }
-    int64_t i = 0;
+    int rs = 0;
     for (int64_t kk = 0; kk < my_ntiles; ++kk) {
         const int64_t tile = int64_t(blockIdx.x) + kk * gridDim.x;
-        for (int j = 0; j < J; ++j, ++i) {
+        for (int j = 0; j < J; ++j) {
             cp_async_wait<kNvlDepth - 1>();
-            V* slot = ring + (i % kNvlDepth) * 3 * kThreads;
-            compute_item<T, false>(p, tile, j, slot, nullptr);
-            const int64_t nx = i + kNvlDepth;
-            if (nx < n_items)
-                issue_item<T>(p, int64_t(blockIdx.x) + (nx / J) * int64_t(gridDim.x), int(nx % J), slot);
+            V* slot = ring + rs * 3 * kThreads;
+            compute_item<T, false>(p, tile, j, slot, nullptr, ring_slot);
+            if (ik < my_ntiles) issue_item<T>(p, int64_t(blockIdx.x) + ik * gridDim.x, ij, slot);
             cp_async_commit();
+            if (++ij == J) ij = 0, ++ik;
+            if (++rs == kNvlDepth) rs = 0;
         }
         // Tiles are published in chunks of kPubChunk: the last producer
         // warp to finish a chunk issues one GPU-scope fence (cumulative
@@ -1186,6 +1236,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     constexpr int E = Tr<T>::EPV;
     extern __shared__ __align__(128) unsigned char dyn_smem[];
     __shared__ SmemCtl sm;
+    __shared__ T* s_ring[kMaxJobs];
     __shared__ __align__(8) uint64_t full[kNvlMaxStages];
     __shared__ __align__(8) uint64_t empty[kNvlMaxStages];
     __shared__ int leaf_base[kMaxPlans + 1];
@@ -1220,6 +1271,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         n_rows_sh = nr;
     }
     if (tid < kMaxVersions) sm.activator[tid] = 0;
+    init_ring_slots<T>(p, s_ring);
     if (tid < kPubRing) pub_count[tid] = 0;
     __syncthreads();
     const int NL = leaf_base[p.n_plans];
@@ -1233,7 +1285,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     if (warp < kWarps) {
         // ---------------- producers ----------------
         const long long pc0 = clock64();
-        my_tiles = nvl_produce<T, kNvlDepth>(p, ring, my_ntiles, pub_count);
+        my_tiles = nvl_produce<T, kNvlDepth>(p, ring, my_ntiles, pub_count, s_ring);
         if (p.prof && tid == 0) p.prof[blockIdx.x * 8 + 0] = clock64() - pc0;
     } else if (warp == 2 * kWarps) {
         // ---------------- puller ----------------
@@ -1465,6 +1517,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     constexpr int E = Tr<T>::EPV;
     extern __shared__ __align__(128) unsigned char dyn_smem[];
     __shared__ SmemCtl sm;
+    __shared__ T* s_ring[kMaxJobs];
     __shared__ __align__(8) uint64_t fullA[kNvlMaxStages], emptyA[kNvlMaxStages];
     __shared__ __align__(8) uint64_t fullB[kNvlMaxStages], emptyB[kNvlMaxStages];
     __shared__ int64_t metaA_tile[kNvlMaxStages], metaB_tile[kNvlMaxStages];
@@ -1517,6 +1570,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         plan_rows[NP] = rows;
     }
     if (tid < kMaxVersions) sm.activator[tid] = 0;
+    init_ring_slots<T>(p, s_ring);
     if (tid < kPubRing) pub_count[tid] = 0;
     if (tid < kRedRing) red_count[tid] = 0;
     __syncthreads();
@@ -1550,7 +1604,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         if (p.prof) p.prof[blockIdx.x * 16 + slot] = v;
     };
     if (warp < kWarps) {
-        my_tiles = nvl_produce<T, kSplitDepth>(p, ring, my_ntiles, pub_count);
+        my_tiles = nvl_produce<T, kSplitDepth>(p, ring, my_ntiles, pub_count, s_ring);
         if (tid == 0) prof_set(0, clock64() - t_start);
     } else if (warp == kWarps) {
         // ---------------- stream A puller ----------------
