@@ -123,6 +123,17 @@ __global__ void tma_multi_kernel(Srcs srcs, int nsrc, size_t bytes_per_src, floa
     if (acc == 1234.5f) out[0] = acc;
 }
 
+// all-to-all push: every thread stores 16-B vectors into the peers' buffers
+struct Dsts { float4* p[8]; };
+__global__ void push_multi_kernel(Dsts dsts, int ndst, size_t n16_per_dst) {
+    const size_t total = n16_per_dst * ndst;
+    const float4 v = make_float4(1.f, 2.f, 3.f, float(threadIdx.x));
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+        const size_t chunk = i / 1024;  // 16 KB chunks round-robin over the peers
+        dsts.p[chunk % ndst][(chunk / ndst) * 1024 + (i % 1024)] = v;
+    }
+}
+
 // HBM streaming copy, to load the memory system while the pulls run
 __global__ void hbm_copy_kernel(const float4* a, float4* b, size_t n16) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n16; i += size_t(gridDim.x) * blockDim.x)
@@ -159,6 +170,28 @@ static int all_to_all(int n, size_t bytes, bool with_hbm) {
         cudaEventCreate(&a[g]); cudaEventCreate(&b[g]); cudaEventCreate(&c[g]); cudaEventCreate(&d[g]);
         cudaStreamCreateWithFlags(&s1[g], cudaStreamNonBlocking);
         cudaStreamCreateWithFlags(&s2[g], cudaStreamNonBlocking);
+    }
+    // push: every GPU writes `bytes` into each peer at once
+    for (int rep = 0; rep < 3; ++rep) {
+        for (int g = 0; g < n; ++g) {
+            CK(cudaSetDevice(g));
+            Dsts dsts;
+            int k = 0;
+            for (int q = 0; q < n; ++q)
+                if (q != g) dsts.p[k++] = reinterpret_cast<float4*>(buf[q]);
+            cudaEventRecord(a[g], s1[g]);
+            push_multi_kernel<<<sms * 4, 256, 0, s1[g]>>>(dsts, n - 1, bytes / 16 / n);
+            cudaEventRecord(b[g], s1[g]);
+        }
+        for (int g = 0; g < n; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaDeviceSynchronize());
+            CK(cudaGetLastError());
+            float ms;
+            cudaEventElapsedTime(&ms, a[g], b[g]);
+            if (rep == 2 && !with_hbm)
+                printf("a2a push n=%d gpu %d: %.3f ms %.1f GB/s egress\n", n, g, ms, (bytes / n) * (n - 1) / ms / 1e6);
+        }
     }
     for (int rep = 0; rep < 3; ++rep) {
         for (int g = 0; g < n; ++g) {
