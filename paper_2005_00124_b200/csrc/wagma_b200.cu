@@ -148,6 +148,7 @@ struct LaunchParams {
     int32_t nvl_stages;   // leaf-ring stages of the multi-GPU TMA kernel
     int32_t split_stages; // reduced-tile ring stages of the split kernel
     int32_t split_span;   // minimum GPUs a group must span to be summed split
+    int32_t red_warps;    // split kernel: stream-A reducer warps (4 or 8 of the 12 shared with stream B)
 };
 
 // ---------------------------------------------------------------------------
@@ -1502,7 +1503,14 @@ constexpr int kSplitThreads = 22 * 32;
 #else
 #define WG_PCNT(...)
 #endif
-constexpr int kFinThreads = 4 * 32;
+// Stream A reducers and stream B finishers share 12 warps, split per launch
+// (LaunchParams.red_warps, 4 or 8): B carries (n-1)/n of the tiles of a sum
+// split over n GPUs, A the owned 1/n plus every tile of pulled groups.
+// 0 = by the span (4 reducers when a split group spans >= 4 GPUs).
+#ifndef WG_RED_WARPS
+#define WG_RED_WARPS 0
+#endif
+constexpr int kRoleWarps = 12;
 
 // Owner of a tile of a split sum: rotates along each CTA's tile sequence so
 // every CTA reduces 1/n_owners of its tiles (tile t is the (t / grid)-th tile
@@ -1548,11 +1556,11 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         ready = 0;
         for (int st = 0; st < NSA; ++st) {
             mbar_init(&fullA[st], 1);
-            mbar_init(&emptyA[st], kWarps);
+            mbar_init(&emptyA[st], p.red_warps);
         }
         for (int st = 0; st < NSB; ++st) {
             mbar_init(&fullB[st], 1);
-            mbar_init(&emptyB[st], kFinThreads / 32);
+            mbar_init(&emptyB[st], kRoleWarps - p.red_warps);
         }
         int acc = 0, rows = 0;
         for (int pl = 0; pl < NP; ++pl) {
@@ -1778,9 +1786,11 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             prof_set(1, clock64() - t_start);
             WG_PCNT(prof_set(8, a_empty); prof_set(9, a_poll); prof_set(10, a_batches);)
         }
-    } else if (warp <= 2 * kWarps) {
+    } else if (warp <= kWarps + p.red_warps) {
         // ---------------- stream A reducers ----------------
-        const int ctid = tid - (kWarps + 1) * 32;
+        const int rtid = tid - (kWarps + 1) * 32;
+        const int ctid = rtid;  // first vector of this thread
+        const int red_threads = p.red_warps * 32;
         while (ready == 0) __nanosleep(64);
         long long wait_a = 0;
         for (int64_t kA = 0; ready == 1; ++kA) {
@@ -1794,18 +1804,21 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             const int64_t tile = metaA_tile[st];
             if (tile < 0) break;
             const unsigned mask = metaA_mask[st];
-            const int64_t idx = tile * p.tile_elems + int64_t(ctid) * E;
             const V* lb = ringA + size_t(st) * NR * kThreads;
             bool owned = false;
+#pragma unroll 1
+            for (int h = 0; h < kThreads / red_threads; ++h) {
+            const int vec = rtid + h * red_threads;
+            const int64_t idx = tile * p.tile_elems + int64_t(vec) * E;
             for (int pl = 0; pl < NP; ++pl) {
                 if (!(mask >> pl & 1)) continue;
                 const DevPlan& P_ = p.plans[pl];
                 // local leaves from L2 (.cg: never a stale L1 line of a reused slot)
                 const int base = leaf_base[pl];
                 auto fetch = [&](int leaf) -> V {
-                    if (WG_SPLIT_TMA_LOCAL) return lb[(base + leaf) * kThreads + ctid];  // row == leaf index
+                    if (WG_SPLIT_TMA_LOCAL) return lb[(base + leaf) * kThreads + vec];  // row == leaf index
                     const int r = row_of[pl][leaf];
-                    if (r >= 0) return lb[r * kThreads + ctid];
+                    if (r >= 0) return lb[r * kThreads + vec];
                     return __ldcg(reinterpret_cast<const V*>(
                         ring_ptr<T>(p, P_.leaves[leaf], sm.leaf_slot[pl][leaf]) + idx));
                 };
@@ -1821,6 +1834,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 };
                 finish_members<T>(p, sm, P_, acc, idx, own_wp);
             }
+            }
             if (owned) {
                 // the last reducer warp of the tile: one fence, then the flags
                 __syncwarp();
@@ -1831,10 +1845,10 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                                  : "=r"(old)
                                  : "r"(smem_u32(cnt))
                                  : "memory");
-                    if (old == kWarps - 1) *cnt = 0;
+                    if (old == unsigned(p.red_warps - 1)) *cnt = 0;
                 }
                 old = __shfl_sync(0xffffffffu, old, 0);
-                if (old == kWarps - 1) {
+                if (old == unsigned(p.red_warps - 1)) {
                     if (p.fence_scope == 0)
                         fence_sys();
                     else
@@ -1853,7 +1867,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             prof_set(3, wait_a);
             prof_set(4, clock64() - t_start);
         }
-    } else if (warp == 2 * kWarps + 1) {
+    } else if (warp == kWarps + p.red_warps + 1) {
         // ---------------- stream B puller ----------------
         // Batches of up to kPullBatch tiles reduced on other GPUs: all the
         // owners' reduced-tile flags loaded at once, then tile by tile (in
@@ -1958,7 +1972,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         }
     } else {
         // ---------------- stream B finishers (2 vectors per thread) ----------------
-        const int ftid = tid - (2 * kWarps + 2) * 32;
+        const int ftid = tid - (kWarps + p.red_warps + 2) * 32;
+        const int fin_threads = (kRoleWarps - p.red_warps) * 32;
         while (ready == 0) __nanosleep(64);
         long long wait_b = 0;
         for (int64_t kB = 0; ready == 1; ++kB) {
@@ -1973,8 +1988,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             if (tile < 0) break;
             const unsigned mask = metaB_mask[st];
             const V* lb = ringB + size_t(st) * NP * kThreads;
-            for (int h = 0; h < kThreads / kFinThreads; ++h) {
-                const int vec = ftid + h * kFinThreads;
+            for (int h = 0; h < kThreads / fin_threads; ++h) {
+                const int vec = ftid + h * fin_threads;
                 const int64_t idx = tile * p.tile_elems + int64_t(vec) * E;
                 for (int pl = 0; pl < NP; ++pl) {
                     if (!(mask >> pl & 1)) continue;
@@ -2605,6 +2620,13 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
             return fail(WG_EINVAL, "split launch does not fit shared memory (%d leaves)", n_leaves_total);
         p.nvl_stages = nsa;
         p.split_stages = nsb;
+        int span_max = 0;
+        for (int k = 0; k < p.n_plans; ++k) {
+            unsigned gpus = 0;
+            for (int li = 0; li < p.plans[k].n_leaves; ++li) gpus |= 1u << (p.plans[k].leaves[li] / ctx->R);
+            span_max = std::max(span_max, __builtin_popcount(gpus));
+        }
+        p.red_warps = WG_RED_WARPS ? WG_RED_WARPS : (span_max >= 4 ? 4 : 8);
         const size_t smem_split = fixed + size_t(nsa) * n_rows_split * row;
         const int di = c.dtype == WG_F32 ? 0 : 1;
         if (ctx->occ_split[di] <= 0) {
