@@ -151,6 +151,20 @@ def batch(ctx: DeviceContext):
 DeviceContext.batch = batch  # type: ignore[attr-defined]
 
 
+def activation_acts(rank: int, root: int, P: int) -> int:
+    """ACT messages `rank` sends in the binomial activation tree rooted at `root`.
+
+    The root sends on every tree edge j < log2 P (collective.py:263-268); rank
+    root ^ q receives at hop msb(q) and forwards on the edges above it
+    (:270-274). -1 (no activation) sends none.
+    """
+    if root < 0:
+        return 0
+    depth = P.bit_length() - 1
+    q = rank ^ root
+    return depth if q == 0 else depth - q.bit_length()
+
+
 class GroupAllreduce:
     """Per-process endpoint of the wait-avoiding group allreduce (collective.py:135-345).
 
@@ -192,19 +206,13 @@ class GroupAllreduce:
         # at the activating rank, one PHASE message per butterfly phase
         self.acts_sent = 0
         self.phases_sent = 0
-        self._tree_depth = P.bit_length() - 1
         self._group_phases = S.bit_length() - 1
 
     def install_fresh(self, vec, iteration: int) -> None:
         self.send_buffer.install(vec, iteration)
 
     def _acts_for(self, root: int) -> int:
-        # the root sends on every tree edge j < log2 P (collective.py:263-268);
-        # rank root ^ q receives at hop msb(q) and forwards on j > hop (:270-274)
-        if root < 0:
-            return 0
-        q = self.rank ^ root
-        return self._tree_depth if q == 0 else self._tree_depth - q.bit_length()
+        return activation_acts(self.rank, root, self.P)
 
     def handle_message(self, src: int, body: bytes) -> None:
         """The reference's transport hook (collective.py:226-233). Device memory

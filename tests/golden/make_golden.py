@@ -13,6 +13,9 @@ the GPU box ever needs the reference:
   collective.npz    group-round accumulators produced by the reference's
                     own `GroupAllreduce` endpoints on its `Simulator`
                     (all-timely, stale/late, literal rule, sync).
+  activation.json   per-rank ACT / PHASE message counters of one version
+                    activated by a single root (`collective.py:182-184`,
+                    `:263-274`, `:319`) for every root, P <= 16.
   training_*.npz    `run_training` trajectories with the per-(rank, t)
                     gradients, the contribution log (rank, version, stamp)
                     captured from `optim._ContributionSink.append`
@@ -343,7 +346,34 @@ def make_training():
     return metas
 
 
+def make_activation() -> list:
+    """Counters after one version whose only activator is `root`: the root
+    joins at t=0, every other rank long after the ACT tree and the phases ran."""
+    out = []
+    for P in (2, 4, 8, 16):
+        for S in (2, 4):
+            if S > P:
+                continue
+            for root in range(P):
+                sim = Simulator(P, link_latency_ms=1.0)
+                nodes = [_Node(sim, r, P, S, np.zeros(3)) for r in range(P)]
+                for r in range(P):
+                    when = 0.0 if r == root else 1000.0
+                    sim.call_at(when, r, (lambda rr=r: nodes[rr].group.join_or_check(0, np.ones(3) * rr)))
+                sim.run_until_idle()
+                out.append({"P": P, "S": S, "root": root,
+                            "acts_sent": [n.group.acts_sent for n in nodes],
+                            "activations_originated": [n.group.activations_originated for n in nodes],
+                            "phases_sent": [n.group.phases_sent for n in nodes]})
+    return out
+
+
 def main():
+    act = make_activation()
+    with open(os.path.join(HERE, "activation.json"), "w") as fp:
+        json.dump(act, fp, separators=(",", ":"))
+    if sys.argv[1:] == ["activation"]:
+        return
     topo = make_topology()
     with open(os.path.join(HERE, "topology.json"), "w") as fp:
         json.dump(topo, fp, separators=(",", ":"))

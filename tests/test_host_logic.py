@@ -92,3 +92,21 @@ def test_tick_schedule_properties(P, T, tau, k, dt):
             done[r].append(t)
     for r in range(P):
         assert done[r] == list(range(T))  # every rank runs every iteration once, in order
+
+
+def test_activation_message_counts_match_reference():
+    """Per-rank ACT counts of a single-root activation, against the reference's
+    own endpoints on its simulator (tests/golden/activation.json)."""
+    import json
+
+    from conftest import GOLDEN
+    from paper_2005_00124_b200.collective import activation_acts
+
+    cases = json.load(open(os.path.join(GOLDEN, "activation.json")))
+    assert len(cases) >= 50
+    for c in cases:
+        P, S, root = c["P"], c["S"], c["root"]
+        assert [activation_acts(r, root, P) for r in range(P)] == c["acts_sent"], c
+        assert sum(c["acts_sent"]) == P - 1
+        assert c["activations_originated"] == [int(r == root) for r in range(P)]
+        assert c["phases_sent"] == [S.bit_length() - 1] * P
