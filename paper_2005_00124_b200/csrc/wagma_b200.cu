@@ -1529,23 +1529,31 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     __shared__ __align__(8) uint64_t fullA[kNvlMaxStages], emptyA[kNvlMaxStages];
     __shared__ __align__(8) uint64_t fullB[kNvlMaxStages], emptyB[kNvlMaxStages];
     __shared__ int64_t metaA_tile[kNvlMaxStages], metaB_tile[kNvlMaxStages];
+    __shared__ int metaA_kc[kNvlMaxStages], metaB_kc[kNvlMaxStages];  // CTA-local tile index
+    // per (plan, owner index): reduced-tile ring and flags of that owner, and
+    // whether it lives on another GPU (no 64-bit division per tile)
+    __shared__ T* s_red_base[kMaxPlans][kSplitMaxP];
+    __shared__ int64_t* s_red_flag[kMaxPlans][kSplitMaxP];
+    __shared__ int8_t s_owner_remote[kMaxPlans][kSplitMaxP];
+    __shared__ const T* s_leaf_src[kMaxPoll / kWarps];  // flat leaf -> its send-ring slot
+    __shared__ const int64_t* s_poll_ptr[kMaxPoll];     // (leaf, warp) flag of tile 0
     __shared__ unsigned metaA_mask[kNvlMaxStages], metaB_mask[kNvlMaxStages];
     __shared__ int leaf_base[kMaxPlans + 1];
     __shared__ int8_t row_of[kMaxPlans][kMaxLeaves];  // stage row of a leaf, -1: read from L2
     __shared__ int plan_rows[kMaxPlans + 1];
     __shared__ volatile int ready;
-    __shared__ int16_t poll_q[kMaxPoll];
-    __shared__ int8_t poll_w[kMaxPoll];
     __shared__ int64_t poll_s[kMaxPoll];
     __shared__ int plan_poll_base[kMaxPlans], plan_poll_cnt[kMaxPlans];
     __shared__ unsigned pub_count[kPubRing];
     __shared__ unsigned red_count[kRedRing];
     __shared__ int64_t bt_tile[kPullBatch];
+    __shared__ int bt_kc[kPullBatch];
     __shared__ unsigned bt_mask[kPullBatch];
     __shared__ int bt_n;
     __shared__ int cell_pref[kPullBatch * kMaxPlans + 1];
     __shared__ int plan_split[kMaxPlans];
     __shared__ int64_t btB_tile[kPullBatch];
+    __shared__ int btB_kc[kPullBatch];
     __shared__ unsigned btB_mask[kPullBatch];
     __shared__ int btB_n;
     const int tid = threadIdx.x;
@@ -1581,6 +1589,15 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     init_ring_slots<T>(p, s_ring);
     if (tid < kPubRing) pub_count[tid] = 0;
     if (tid < kRedRing) red_count[tid] = 0;
+    if (tid < NP * kSplitMaxP) {
+        const int pl = tid / kSplitMaxP, oi = tid % kSplitMaxP;
+        if (oi < p.owners[pl].n) {
+            const int owner = p.owners[pl].rank[oi];
+            s_red_base[pl][oi] = red_ptr<T>(p, owner, p.versions[p.plans[pl].vidx].version);
+            s_red_flag[pl][oi] = red_flag_ptr(p, owner, 0);
+            s_owner_remote[pl][oi] = int8_t(owner / p.R != p.gpu_index);
+        }
+    }
     __syncthreads();
     const int NL = leaf_base[NP];
     const int NR = plan_rows[NP];  // stage rows: leaves copied by TMA
@@ -1591,11 +1608,10 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     const unsigned tile_bytes = unsigned(p.tile_elems * int64_t(sizeof(T)));
     unsigned my_tiles = 0;
     // plans of a tile handled by stream A (mask A) or stream B (mask B)
-    auto masks = [&](int64_t tile, unsigned& ma, unsigned& mb) {
+    auto masks = [&](int kc, unsigned& ma, unsigned& mb) {
         ma = mb = 0;
         for (int pl = 0; pl < NP; ++pl) {
-            const DevPlan& P_ = p.plans[pl];
-            const bool remote_owner = plan_split[pl] && split_owner(p, pl, tile) / p.R != p.gpu_index;
+            const bool remote_owner = plan_split[pl] && s_owner_remote[pl][kc % p.owners[pl].n];
             (remote_owner ? mb : ma) |= 1u << pl;
         }
     };
@@ -1646,14 +1662,15 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                             raise_error(p, WG_EINVAL, n_poll);
                             break;
                         }
-                        poll_q[n_poll] = int16_t(q);
-                        poll_w[n_poll] = int8_t(w);
+                        s_poll_ptr[n_poll] = flag_ptr(p, q, 0, w);
                         poll_s[n_poll] = sm.stamps[P_.vidx][q];
                         ++n_poll;
                     }
                 }
                 plan_poll_cnt[pl] = n_poll - plan_poll_base[pl];
                 plan_split[pl] = split && remote;
+                for (int li = 0; li < P_.n_leaves; ++li)
+                    s_leaf_src[leaf_base[pl] + li] = ring_ptr<T>(p, P_.leaves[li], sm.leaf_slot[pl][li]);
             }
             __threadfence_block();
 #ifdef WG_PROF_NOCONSUME  // profiling only: producers alone (results are garbage)
@@ -1668,7 +1685,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         resolved = resolved && ready == 1;
         int batch = NSA - 1 < kPullBatch ? (NSA > 1 ? NSA - 1 : 1) : kPullBatch;
         if (WG_SPLIT_ABATCH > 0 && WG_SPLIT_ABATCH < batch) batch = WG_SPLIT_ABATCH;
-        int64_t kA = 0, kc = 0;
+        int64_t kA = 0;
+        int kc = 0, stA = 0, phA = 0;  // stage and phase of tile kA (no division per tile)
         bool ok = resolved;
         WG_PCNT(long long a_empty = 0, a_poll = 0, a_batches = 0;)
         while (ok) {
@@ -1676,14 +1694,15 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             if (lane == 0) {
                 int n = 0;
                 while (kc < my_ntiles && n < batch) {
-                    const int64_t tile = int64_t(blockIdx.x) + kc * gridDim.x;
                     unsigned ma, mb;
-                    masks(tile, ma, mb);
+                    masks(kc, ma, mb);
+                    if (ma) {
+                        bt_tile[n] = int64_t(blockIdx.x) + int64_t(kc) * gridDim.x;
+                        bt_kc[n] = kc;
+                        bt_mask[n] = ma;
+                        ++n;
+                    }
                     ++kc;
-                    if (!ma) continue;
-                    bt_tile[n] = tile;
-                    bt_mask[n] = ma;
-                    ++n;
                 }
                 bt_n = n;
             }
@@ -1692,9 +1711,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             const int nb = bt_n;
             if (nb == 0) break;
             WG_PCNT(long long c0 = clock64();)
-            for (int b = 0; b < nb && ok; ++b) {
-                const int64_t k = kA + b;
-                if (k >= NSA && !mbar_wait(p, &emptyA[k % NSA], unsigned((k / NSA - 1) & 1))) ok = false;
+            for (int b = 0, st = stA, ph = phA; b < nb && ok; ++b) {
+                if (kA + b >= NSA && !mbar_wait(p, &emptyA[st], unsigned(ph ^ 1))) ok = false;
+                if (++st == NSA) st = 0, ph ^= 1;
             }
             WG_PCNT(a_empty += clock64() - c0; c0 = clock64(); ++a_batches;)
             if (!ok) {
@@ -1726,7 +1745,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                     int c = 0;
                     while (cell_pref[c + 1] <= e) ++c;
                     const int idx = plan_poll_base[c % NP] + (e - cell_pref[c]);
-                    fp[r] = flag_ptr(p, poll_q[idx], bt_tile[c / NP], poll_w[idx]);
+                    fp[r] = s_poll_ptr[idx] + bt_tile[c / NP] * kWarps;
                     want[r] = poll_s[idx];
                     v[r] = ld_relaxed_sys(fp[r]);
                 }
@@ -1751,14 +1770,15 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             WG_PCNT(a_poll += clock64() - c0;)
             acquire_for_tma();
             if (lane == 0) {
-                for (int b = 0; b < nb; ++b) {
-                    const int st = int((kA + b) % NSA);
+                for (int b = 0, st = stA; b < nb; ++b) {
                     unsigned rows = 0;
                     for (int pl = 0; pl < NP; ++pl)
                         if (bt_mask[b] >> pl & 1) rows += plan_rows[pl];
                     metaA_tile[st] = bt_tile[b];
+                    metaA_kc[st] = bt_kc[b];
                     metaA_mask[st] = bt_mask[b];
                     mbar_arrive_expect_tx(&fullA[st], rows * tile_bytes);
+                    if (++st == NSA) st = 0;
                 }
             }
             __syncwarp();
@@ -1770,19 +1790,20 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 const int li = f - leaf_base[pl];
                 const int r = row_of[pl][li];
                 if (r < 0) continue;
-                const int st = int((kA + b) % NSA);
-                const T* src =
-                    ring_ptr<T>(p, p.plans[pl].leaves[li], sm.leaf_slot[pl][li]) + bt_tile[b] * p.tile_elems;
+                const int st = stA + b < NSA ? stA + b : stA + b - NSA;
+                const T* src = s_leaf_src[f] + bt_tile[b] * p.tile_elems;
                 bulk_g2s(ringA + (size_t(st) * NR + r) * kThreads, src, tile_bytes, &fullA[st]);
             }
             __syncwarp();
             kA += nb;
+            stA += nb;
+            if (stA >= NSA) stA -= NSA, phA ^= 1;
         }
         // end of stream A
-        if (kA >= NSA && !mbar_wait(p, &emptyA[kA % NSA], unsigned((kA / NSA - 1) & 1))) ok = false;
+        if (kA >= NSA && !mbar_wait(p, &emptyA[stA], unsigned(phA ^ 1))) ok = false;
         if (lane == 0) {
-            metaA_tile[kA % NSA] = -1;
-            mbar_arrive(&fullA[kA % NSA]);
+            metaA_tile[stA] = -1;
+            mbar_arrive(&fullA[stA]);
             prof_set(1, clock64() - t_start);
             WG_PCNT(prof_set(8, a_empty); prof_set(9, a_poll); prof_set(10, a_batches);)
         }
@@ -1793,10 +1814,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         const int red_threads = p.red_warps * 32;
         while (ready == 0) __nanosleep(64);
         long long wait_a = 0;
-        for (int64_t kA = 0; ready == 1; ++kA) {
-            const int st = int(kA % NSA);
+        for (int64_t kA = 0, st = 0, ph = 0; ready == 1; ++kA) {
             const long long w0 = clock64();
-            if (!mbar_wait(p, &fullA[st], unsigned((kA / NSA) & 1))) {
+            if (!mbar_wait(p, &fullA[st], unsigned(ph))) {
                 if (lane == 0) raise_error(p, WG_ETIMEOUT, kA);
                 break;
             }
@@ -1804,6 +1824,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             const int64_t tile = metaA_tile[st];
             if (tile < 0) break;
             const unsigned mask = metaA_mask[st];
+            const int kc = metaA_kc[st];
             const V* lb = ringA + size_t(st) * NR * kThreads;
             bool owned = false;
 #pragma unroll 1
@@ -1824,8 +1845,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 };
                 const V acc = tree_sum<T>(fetch, P_.log_leaves);
                 if (plan_split[pl]) {  // this GPU owns the tile: publish the reduced tile
-                    __stcg(reinterpret_cast<V*>(red_ptr<T>(p, split_owner(p, pl, tile),
-                                                          p.versions[P_.vidx].version) + idx), acc);
+                    __stcg(reinterpret_cast<V*>(s_red_base[pl][kc % p.owners[pl].n] + idx), acc);
                     owned = true;
                 }
                 auto own_wp = [&](int j) -> V {
@@ -1853,15 +1873,14 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                         fence_sys();
                     else
                         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    if (lane < NP && (mask >> lane & 1) && plan_split[lane]) {
-                        const DevPlan& P_ = p.plans[lane];
-                        st_relaxed_sys(red_flag_ptr(p, split_owner(p, lane, tile), tile),
-                                       p.versions[P_.vidx].version);
-                    }
+                    if (lane < NP && (mask >> lane & 1) && plan_split[lane])
+                        st_relaxed_sys(s_red_flag[lane][kc % p.owners[lane].n] + tile,
+                                       p.versions[p.plans[lane].vidx].version);
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&emptyA[st]);
+            if (++st == NSA) st = 0, ph ^= 1;
         }
         if (ctid == 0) {
             prof_set(3, wait_a);
@@ -1873,7 +1892,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         // owners' reduced-tile flags loaded at once, then tile by tile (in
         // order) wait, copy the reduced tiles.
         while (ready == 0) __nanosleep(64);
-        int64_t kB = 0, kc = 0;
+        int64_t kB = 0;
+        int kc = 0, stB = 0, phB = 0;
         bool ok = ready == 1;
         WG_PCNT(long long b_empty = 0, b_poll = 0, b_notready = 0;)
         int batch = NSB - 1 < kPullBatch ? (NSB > 1 ? NSB - 1 : 1) : kPullBatch;
@@ -1882,14 +1902,15 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             if (lane == 0) {
                 int n = 0;
                 while (kc < my_ntiles && n < batch) {
-                    const int64_t tile = int64_t(blockIdx.x) + kc * gridDim.x;
                     unsigned ma, mb;
-                    masks(tile, ma, mb);
+                    masks(kc, ma, mb);
+                    if (mb) {
+                        btB_tile[n] = int64_t(blockIdx.x) + int64_t(kc) * gridDim.x;
+                        btB_kc[n] = kc;
+                        btB_mask[n] = mb;
+                        ++n;
+                    }
                     ++kc;
-                    if (!mb) continue;
-                    btB_tile[n] = tile;
-                    btB_mask[n] = mb;
-                    ++n;
                 }
                 btB_n = n;
             }
@@ -1902,9 +1923,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             const int64_t* fp = nullptr;
             const int e = lane;
             if (e < nb * NP && (btB_mask[e / NP] >> (e % NP) & 1)) {
-                const DevPlan& P_ = p.plans[e % NP];
-                want = p.versions[P_.vidx].version;
-                fp = red_flag_ptr(p, split_owner(p, e % NP, btB_tile[e / NP]), btB_tile[e / NP]);
+                const int pl = e % NP;
+                want = p.versions[p.plans[pl].vidx].version;
+                fp = s_red_flag[pl][btB_kc[e / NP] % p.owners[pl].n] + btB_tile[e / NP];
                 x = ld_relaxed_sys(fp);
             }
             int rc = 0;
@@ -1914,12 +1935,13 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             if (all_ready) acquire_for_tma();
             for (int bb = 0; bb < nb && ok; ++bb) {
                 const int64_t k = kB + bb;
-                const int st = int(k % NSB);
+                const int st = stB;
                 WG_PCNT(long long c0 = clock64();)
-                if (k >= NSB && !mbar_wait(p, &emptyB[st], unsigned((k / NSB - 1) & 1))) {
+                if (k >= NSB && !mbar_wait(p, &emptyB[st], unsigned(phB ^ 1))) {
                     ok = false;
                     break;
                 }
+                if (++stB == NSB) stB = 0, phB ^= 1;
                 WG_PCNT(b_empty += clock64() - c0; c0 = clock64();)
                 if (!all_ready && fp && e / NP == bb) {
                     const uint64_t t0 = globaltimer();
@@ -1950,9 +1972,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 }
                 __syncwarp();
                 if (lane < NP && (mb >> lane & 1)) {
-                    const DevPlan& P_ = p.plans[lane];
-                    const T* src = red_ptr<T>(p, split_owner(p, lane, tile), p.versions[P_.vidx].version) +
-                                   tile * p.tile_elems;
+                    const T* src = s_red_base[lane][btB_kc[bb] % p.owners[lane].n] + tile * p.tile_elems;
                     bulk_g2s(ringB + (size_t(st) * NP + lane) * kThreads, src, tile_bytes, &fullB[st]);
                 }
                 __syncwarp();
@@ -1963,10 +1983,10 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             }
             kB += nb;
         }
-        if (kB >= NSB && !mbar_wait(p, &emptyB[kB % NSB], unsigned((kB / NSB - 1) & 1))) ok = false;
+        if (kB >= NSB && !mbar_wait(p, &emptyB[stB], unsigned(phB ^ 1))) ok = false;
         if (lane == 0) {
-            metaB_tile[kB % NSB] = -1;
-            mbar_arrive(&fullB[kB % NSB]);
+            metaB_tile[stB] = -1;
+            mbar_arrive(&fullB[stB]);
             prof_set(5, clock64() - t_start);
             WG_PCNT(prof_set(11, b_empty); prof_set(12, b_poll); prof_set(13, b_notready);)
         }
@@ -1976,10 +1996,10 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         const int fin_threads = (kRoleWarps - p.red_warps) * 32;
         while (ready == 0) __nanosleep(64);
         long long wait_b = 0;
-        for (int64_t kB = 0; ready == 1; ++kB) {
-            const int st = int(kB % NSB);
+        WG_PCNT(long long fin_work = 0; const long long ready_at = clock64() - t_start;)
+        for (int64_t kB = 0, st = 0, ph = 0; ready == 1; ++kB) {
             const long long w0 = clock64();
-            if (!mbar_wait(p, &fullB[st], unsigned((kB / NSB) & 1))) {
+            if (!mbar_wait(p, &fullB[st], unsigned(ph))) {
                 if (lane == 0) raise_error(p, WG_ETIMEOUT, kB);
                 break;
             }
@@ -1988,6 +2008,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             if (tile < 0) break;
             const unsigned mask = metaB_mask[st];
             const V* lb = ringB + size_t(st) * NP * kThreads;
+            WG_PCNT(const long long f0 = clock64();)
             for (int h = 0; h < kThreads / fin_threads; ++h) {
                 const int vec = ftid + h * fin_threads;
                 const int64_t idx = tile * p.tile_elems + int64_t(vec) * E;
@@ -2002,11 +2023,14 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 }
             }
             __syncwarp();
+            WG_PCNT(fin_work += clock64() - f0;)
             if (lane == 0) mbar_arrive(&emptyB[st]);
+            if (++st == NSB) st = 0, ph ^= 1;
         }
         if (ftid == 0) {
             prof_set(6, wait_b);
             prof_set(7, clock64() - t_start);
+            WG_PCNT(prof_set(14, ready_at); prof_set(15, fin_work);)
         }
     }
     if (aborted(p)) sm.abort = 1;

@@ -53,7 +53,7 @@ for t in range(a.iters):
         split_prof = os.environ.get("WG_PROF_SPLIT", "0") == "1"
         p = prof.view(-1, 16 if split_prof else 8).cpu().numpy().astype(np.float64)
         if os.environ.get("WG_PROF_SPLIT", "0") == "1":
-            names = ["producer_total", "pullA_total", "x", "redA_full_wait", "redA_total", "pullB_total", "finB_full_wait", "finB_total", "pullA_empty", "pullA_poll", "x", "pullB_empty", "pullB_poll", "x", "x", "x"]
+            names = ["producer_total", "pullA_total", "x", "redA_full_wait", "redA_total", "pullB_total", "finB_full_wait", "finB_total", "pullA_empty", "pullA_poll", "x", "pullB_empty", "pullB_poll", "x", "fin_ready_at", "fin_work"]
         elif os.environ.get("WG_NVL", "1") != "0":
             names = ["producer_total", "pull_empty_wait", "pull_poll", "pull_issue", "cons_full_wait", "x", "cons_total", "cons_ready_wait"]
         else:
