@@ -1855,9 +1855,12 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 finish_members<T>(p, sm, P_, acc, idx, own_wp);
             }
             }
+            // the stage is free once every lane has read it: release it before
+            // the (slow) fence below so the puller refills it meanwhile
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&emptyA[st]);
             if (owned) {
                 // the last reducer warp of the tile: one fence, then the flags
-                __syncwarp();
                 unsigned old = 0;
                 if (lane == 0) {
                     unsigned* cnt = &red_count[kA & (kRedRing - 1)];
@@ -1878,8 +1881,6 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                                        p.versions[p.plans[lane].vidx].version);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&emptyA[st]);
             if (++st == NSA) st = 0, ph ^= 1;
         }
         if (ctid == 0) {
