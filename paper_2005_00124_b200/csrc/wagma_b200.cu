@@ -1496,7 +1496,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
 // Stream A never waits on stream B, so no cross-GPU wait cycle exists.
 // ---------------------------------------------------------------------------
 
-constexpr int kSplitThreads = 22 * 32;
+constexpr int kSplitThreads = 23 * 32;  // + 1 publisher warp (reduced-tile fences and flags)
 // puller wait counters for tools/phase_profile.py (off: they cost registers)
 #ifdef WG_PROF_COUNTERS
 #define WG_PCNT(...) __VA_ARGS__
@@ -1546,6 +1546,12 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     __shared__ int plan_poll_base[kMaxPlans], plan_poll_cnt[kMaxPlans];
     __shared__ unsigned pub_count[kPubRing];
     __shared__ unsigned red_count[kRedRing];
+    // owned reduced tiles handed from the reducers to the publisher warp
+    __shared__ int64_t pubq_tile[kRedRing];
+    __shared__ int pubq_kc[kRedRing];
+    __shared__ unsigned pubq_mask[kRedRing];
+    __shared__ int64_t pubq_seq[kRedRing];
+    __shared__ volatile int64_t pub_done, pub_end;
     __shared__ int64_t bt_tile[kPullBatch];
     __shared__ int bt_kc[kPullBatch];
     __shared__ unsigned bt_mask[kPullBatch];
@@ -1588,7 +1594,14 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     if (tid < kMaxVersions) sm.activator[tid] = 0;
     init_ring_slots<T>(p, s_ring);
     if (tid < kPubRing) pub_count[tid] = 0;
-    if (tid < kRedRing) red_count[tid] = 0;
+    if (tid < kRedRing) {
+        red_count[tid] = 0;
+        pubq_seq[tid] = -1;
+    }
+    if (tid == 0) {
+        pub_done = 0;
+        pub_end = -1;
+    }
     if (tid < NP * kSplitMaxP) {
         const int pl = tid / kSplitMaxP, oi = tid % kSplitMaxP;
         if (oi < p.owners[pl].n) {
@@ -1814,6 +1827,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         const int red_threads = p.red_warps * 32;
         while (ready == 0) __nanosleep(64);
         long long wait_a = 0;
+        int64_t oq = 0;  // owned tiles so far (same count in every reducer warp)
         for (int64_t kA = 0, st = 0, ph = 0; ready == 1; ++kA) {
             const long long w0 = clock64();
             if (!mbar_wait(p, &fullA[st], unsigned(ph))) {
@@ -1860,30 +1874,39 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             __syncwarp();
             if (lane == 0) mbar_arrive(&emptyA[st]);
             if (owned) {
-                // the last reducer warp of the tile: one fence, then the flags
-                unsigned old = 0;
+                // the last reducer warp of the tile hands it to the publisher
+                // (which fences and raises the flags, off the reducers' path)
                 if (lane == 0) {
                     unsigned* cnt = &red_count[kA & (kRedRing - 1)];
+                    unsigned old;
                     asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                                  : "=r"(old)
                                  : "r"(smem_u32(cnt))
                                  : "memory");
-                    if (old == unsigned(p.red_warps - 1)) *cnt = 0;
+                    if (old == unsigned(p.red_warps - 1)) {
+                        *cnt = 0;
+                        const uint64_t t0 = globaltimer();
+                        while (pub_done <= oq - kRedRing) {  // queue full: publisher lags
+                            if (globaltimer() - t0 > uint64_t(p.timeout_ns) || aborted(p)) break;
+                            __nanosleep(64);
+                        }
+                        const int slot = int(oq & (kRedRing - 1));
+                        unsigned ms = 0;
+                        for (int pl = 0; pl < NP; ++pl) ms |= (mask >> pl & 1) && plan_split[pl] ? 1u << pl : 0u;
+                        pubq_tile[slot] = tile;
+                        pubq_kc[slot] = kc;
+                        pubq_mask[slot] = ms;
+                        asm volatile("st.release.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&pubq_seq[slot])),
+                                     "l"(oq)
+                                     : "memory");
+                    }
                 }
-                old = __shfl_sync(0xffffffffu, old, 0);
-                if (old == unsigned(p.red_warps - 1)) {
-                    if (p.fence_scope == 0)
-                        fence_sys();
-                    else
-                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    if (lane < NP && (mask >> lane & 1) && plan_split[lane])
-                        st_relaxed_sys(s_red_flag[lane][kc % p.owners[lane].n] + tile,
-                                       p.versions[p.plans[lane].vidx].version);
-                }
+                ++oq;
             }
             if (++st == NSA) st = 0, ph ^= 1;
         }
         if (ctid == 0) {
+            pub_end = oq;  // every owned tile has been handed over (or the stream stopped)
             prof_set(3, wait_a);
             prof_set(4, clock64() - t_start);
         }
@@ -1990,6 +2013,66 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             mbar_arrive(&fullB[stB]);
             prof_set(5, clock64() - t_start);
             WG_PCNT(prof_set(11, b_empty); prof_set(12, b_poll); prof_set(13, b_notready);)
+        }
+    } else if (warp == kSplitThreads / 32 - 1) {
+        // ---------------- publisher ----------------
+        // Owned reduced tiles, in order: every run of consecutive ready tiles
+        // gets one fence (cumulative over the reducers' stores, acquired
+        // through the queue) and then its flags.
+        while (ready == 0) __nanosleep(64);
+        int64_t next = 0;
+        const uint64_t t0 = globaltimer();
+        while (ready == 1) {
+            int n = 0;
+            if (lane == 0) {
+                for (;;) {
+                    int64_t v;
+                    asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];"
+                                 : "=l"(v)
+                                 : "r"(smem_u32(&pubq_seq[next & (kRedRing - 1)]))
+                                 : "memory");
+                    if (v == next) break;
+                    const int64_t e = pub_end;
+                    if ((e >= 0 && next >= e) || aborted(p)) {
+                        n = -1;
+                        break;
+                    }
+                    if (globaltimer() - t0 > uint64_t(p.timeout_ns)) {
+                        raise_error(p, WG_ETIMEOUT, next);
+                        n = -1;
+                        break;
+                    }
+                    __nanosleep(32);
+                }
+                if (n == 0) {
+                    n = 1;
+                    while (n < kRedRing / 2) {
+                        int64_t v;
+                        asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];"
+                                     : "=l"(v)
+                                     : "r"(smem_u32(&pubq_seq[(next + n) & (kRedRing - 1)]))
+                                     : "memory");
+                        if (v != next + n) break;
+                        ++n;
+                    }
+                }
+            }
+            n = __shfl_sync(0xffffffffu, n, 0);
+            if (n < 0) break;
+            __syncwarp();
+            if (p.fence_scope == 0)
+                fence_sys();
+            else
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            for (int e = lane; e < n * NP; e += 32) {
+                const int slot = int((next + e / NP) & (kRedRing - 1)), pl = e % NP;
+                if (pubq_mask[slot] >> pl & 1)
+                    st_relaxed_sys(s_red_flag[pl][pubq_kc[slot] % p.owners[pl].n] + pubq_tile[slot],
+                                   p.versions[p.plans[pl].vidx].version);
+            }
+            __syncwarp();
+            next += n;
+            if (lane == 0) pub_done = next;
         }
     } else {
         // ---------------- stream B finishers (2 vectors per thread) ----------------
