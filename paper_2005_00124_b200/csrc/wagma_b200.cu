@@ -1242,9 +1242,9 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     __shared__ __align__(8) uint64_t empty[kNvlMaxStages];
     __shared__ int leaf_base[kMaxPlans + 1];
     __shared__ volatile int ready;
-    __shared__ int16_t poll_q[kMaxPoll];
-    __shared__ int8_t poll_w[kMaxPoll];
+    __shared__ const int64_t* s_poll_ptr[kMaxPoll];     // (leaf, warp) flag of tile 0
     __shared__ int64_t poll_s[kMaxPoll];
+    __shared__ const T* s_leaf_src[kMaxPoll / kWarps];  // flat leaf -> its send-ring slot
     __shared__ int n_poll_sh;
     __shared__ int n_rows_sh;
     __shared__ unsigned pub_count[kPubRing];
@@ -1307,12 +1307,14 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
                             raise_error(p, WG_EINVAL, n_poll);
                             break;
                         }
-                        poll_q[n_poll] = int16_t(q);
-                        poll_w[n_poll] = int8_t(w);
+                        s_poll_ptr[n_poll] = flag_ptr(p, q, 0, w);
                         poll_s[n_poll] = sm.stamps[p.plans[pl].vidx][q];
                         ++n_poll;
                     }
                 }
+            for (int pl = 0; pl < p.n_plans; ++pl)
+                for (int li = 0; li < p.plans[pl].n_leaves; ++li)
+                    s_leaf_src[leaf_base[pl] + li] = ring_ptr<T>(p, p.plans[pl].leaves[li], sm.leaf_slot[pl][li]);
             n_poll_sh = n_poll;
             __threadfence_block();
             ready = aborted(p) ? 2 : 1;
@@ -1327,13 +1329,14 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         // the TMA copies of the whole batch.
         const int batch = NS - 1 < kPullBatch ? (NS > 1 ? NS - 1 : 1) : kPullBatch;
         long long cy_empty = 0, cy_poll = 0, cy_issue = 0;
+        int st0 = 0, ph0 = 0;  // stage and phase of tile kc (no division per tile)
         for (int64_t kc = 0; resolved && kc < my_ntiles; kc += batch) {
             const int nb = int(my_ntiles - kc < batch ? my_ntiles - kc : batch);
             bool ok = true;
             long long c0 = clock64();
-            for (int b = 0; b < nb && ok; ++b) {
-                const int64_t k = kc + b;
-                if (k >= NS && !mbar_wait(p, &empty[k % NS], unsigned((k / NS - 1) & 1))) ok = false;
+            for (int b = 0, st = st0, ph = ph0; b < nb && ok; ++b) {
+                if (kc + b >= NS && !mbar_wait(p, &empty[st], unsigned(ph ^ 1))) ok = false;
+                if (++st == NS) st = 0, ph ^= 1;
             }
             long long c1 = clock64();
             cy_empty += c1 - c0;
@@ -1351,7 +1354,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
                     if (e < total) {
                         const int idx = e % n_poll;
                         const int64_t tile = int64_t(blockIdx.x) + (kc + e / n_poll) * gridDim.x;
-                        v[r] = ld_relaxed_sys(flag_ptr(p, poll_q[idx], tile, poll_w[idx]));
+                        v[r] = ld_relaxed_sys(s_poll_ptr[idx] + tile * kWarps);
                     }
                 }
 #pragma unroll
@@ -1368,10 +1371,10 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
                             break;
                         }
                         __nanosleep(32);
-                        v[r] = ld_relaxed_sys(flag_ptr(p, poll_q[idx], tile, poll_w[idx]));
+                        v[r] = ld_relaxed_sys(s_poll_ptr[idx] + tile * kWarps);
                     }
                     if (!rc && v[r] >= poll_s[idx] + p.D) rc = WG_EPROTO;
-                    if (rc) raise_error(p, rc, int64_t(poll_q[idx]) << 32 | (tile & 0xffffffff));
+                    if (rc) raise_error(p, rc, int64_t(idx) << 32 | (tile & 0xffffffff));
                 }
             }
             if (__any_sync(0xffffffffu, rc != 0)) break;
@@ -1387,26 +1390,23 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
             else
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            for (int b = 0; b < nb; ++b) {
-                const int64_t k = kc + b;
-                const int st = int(k % NS);
+            for (int b = 0, st = st0; b < nb; ++b) {
                 if (lane == 0) mbar_arrive_expect_tx(&full[st], unsigned(NR) * tile_bytes);
+                if (++st == NS) st = 0;
             }
             __syncwarp();
             for (int e = lane; e < nb * NL; e += 32) {
                 const int b = e / NL, f = e % NL;
                 const int row = tma_row[f];
                 if (row < 0) continue;
-                int pl = 0;
-                while (leaf_base[pl + 1] <= f) ++pl;
-                const int li = f - leaf_base[pl];
-                const int64_t k = kc + b;
-                const int st = int(k % NS);
-                const int64_t tile = int64_t(blockIdx.x) + k * gridDim.x;
-                const T* src = ring_ptr<T>(p, p.plans[pl].leaves[li], sm.leaf_slot[pl][li]) + tile * p.tile_elems;
+                const int st = st0 + b < NS ? st0 + b : st0 + b - NS;
+                const int64_t tile = int64_t(blockIdx.x) + (kc + b) * gridDim.x;
+                const T* src = s_leaf_src[f] + tile * p.tile_elems;
                 bulk_g2s(leafbuf + (size_t(st) * NR + row) * kThreads, src, tile_bytes, &full[st]);
             }
             __syncwarp();
+            st0 += nb;
+            if (st0 >= NS) st0 -= NS, ph0 ^= 1;
             cy_issue += clock64() - c2;
         }
         if (p.prof && lane == 0) {
@@ -1422,10 +1422,9 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         const long long cc1 = clock64();
         long long cy_full = 0;
         if (ready == 1) {
-            for (int64_t kc = 0; kc < my_ntiles; ++kc) {
-                const int st = int(kc % NS);
+            for (int64_t kc = 0, st = 0, ph = 0; kc < my_ntiles; ++kc) {
                 const long long w0 = clock64();
-                if (!mbar_wait(p, &full[st], unsigned((kc / NS) & 1))) {
+                if (!mbar_wait(p, &full[st], unsigned(ph))) {
                     if (lane == 0) raise_error(p, WG_ETIMEOUT, kc);
                     break;
                 }
@@ -1451,6 +1450,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[st]);
+                if (++st == NS) st = 0, ph ^= 1;
             }
         }
         if (p.prof && ctid == 0) {
