@@ -594,10 +594,11 @@ __device__ __forceinline__ void issue_item(const LaunchParams& p, int64_t tile, 
 // Send-ring slot of every job of the launch (the W' it installs), computed
 // once per CTA instead of a 64-bit modulo per item. Caller syncs after.
 template <typename T>
-__device__ __forceinline__ void init_ring_slots(const LaunchParams& p, T** ring_slot) {
+__device__ __forceinline__ void init_ring_slots(const LaunchParams& p, T** ring_slot, int64_t** flag0 = nullptr) {
     if (threadIdx.x < p.n_jobs) {
         const DevJob& jb = p.jobs[threadIdx.x];
         ring_slot[threadIdx.x] = ring_ptr<T>(p, jb.rank, slot_of(p, jb.version));
+        if (flag0) flag0[threadIdx.x] = flag_ptr(p, jb.rank, 0, 0);  // warp-tile flags of the job's rank
     }
 }
 
@@ -1152,7 +1153,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // stores acquired through the shared-memory counter). Never waits on a peer.
 template <typename T, int kNvlDepth>
 __device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename Tr<T>::V* ring, int64_t my_ntiles,
-                                                unsigned* pub_count, T* const* ring_slot) {
+                                                unsigned* pub_count, T* const* ring_slot,
+                                                int64_t* const* flag_base) {
     using V = typename Tr<T>::V;
     const int lane = threadIdx.x & 31;
     const int J = p.n_jobs;
@@ -1207,7 +1209,7 @@ __device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename 
                     const int w = e % kWarps, j = (e / kWarps) % J, b = e / (kWarps * J);
                     const DevJob& jb = p.jobs[j];
                     if (jb.produces)
-                        st_relaxed_sys(flag_ptr(p, jb.rank, int64_t(blockIdx.x) + (k0 + b) * gridDim.x, w),
+                        st_relaxed_sys(flag_base[j] + (int64_t(blockIdx.x) + (k0 + b) * gridDim.x) * kWarps + w,
                                        jb.version);
                 }
             }
@@ -1238,6 +1240,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     extern __shared__ __align__(128) unsigned char dyn_smem[];
     __shared__ SmemCtl sm;
     __shared__ T* s_ring[kMaxJobs];
+    __shared__ int64_t* s_flag0[kMaxJobs];
     __shared__ __align__(8) uint64_t full[kNvlMaxStages];
     __shared__ __align__(8) uint64_t empty[kNvlMaxStages];
     __shared__ int leaf_base[kMaxPlans + 1];
@@ -1272,7 +1275,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         n_rows_sh = nr;
     }
     if (tid < kMaxVersions) sm.activator[tid] = 0;
-    init_ring_slots<T>(p, s_ring);
+    init_ring_slots<T>(p, s_ring, s_flag0);
     if (tid < kPubRing) pub_count[tid] = 0;
     __syncthreads();
     const int NL = leaf_base[p.n_plans];
@@ -1286,7 +1289,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     if (warp < kWarps) {
         // ---------------- producers ----------------
         const long long pc0 = clock64();
-        my_tiles = nvl_produce<T, kNvlDepth>(p, ring, my_ntiles, pub_count, s_ring);
+        my_tiles = nvl_produce<T, kNvlDepth>(p, ring, my_ntiles, pub_count, s_ring, s_flag0);
         if (p.prof && tid == 0) p.prof[blockIdx.x * 8 + 0] = clock64() - pc0;
     } else if (warp == 2 * kWarps) {
         // ---------------- puller ----------------
@@ -1526,6 +1529,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     extern __shared__ __align__(128) unsigned char dyn_smem[];
     __shared__ SmemCtl sm;
     __shared__ T* s_ring[kMaxJobs];
+    __shared__ int64_t* s_flag0[kMaxJobs];
     __shared__ __align__(8) uint64_t fullA[kNvlMaxStages], emptyA[kNvlMaxStages];
     __shared__ __align__(8) uint64_t fullB[kNvlMaxStages], emptyB[kNvlMaxStages];
     __shared__ int64_t metaA_tile[kNvlMaxStages], metaB_tile[kNvlMaxStages];
@@ -1592,7 +1596,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         plan_rows[NP] = rows;
     }
     if (tid < kMaxVersions) sm.activator[tid] = 0;
-    init_ring_slots<T>(p, s_ring);
+    init_ring_slots<T>(p, s_ring, s_flag0);
     if (tid < kPubRing) pub_count[tid] = 0;
     if (tid < kRedRing) {
         red_count[tid] = 0;
@@ -1641,7 +1645,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         if (p.prof) p.prof[blockIdx.x * 16 + slot] = v;
     };
     if (warp < kWarps) {
-        my_tiles = nvl_produce<T, kSplitDepth>(p, ring, my_ntiles, pub_count, s_ring);
+        my_tiles = nvl_produce<T, kSplitDepth>(p, ring, my_ntiles, pub_count, s_ring, s_flag0);
         if (tid == 0) prof_set(0, clock64() - t_start);
     } else if (warp == kWarps) {
         // ---------------- stream A puller ----------------
