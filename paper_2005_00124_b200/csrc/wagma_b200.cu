@@ -124,7 +124,7 @@ struct DevPlan {
     int8_t members[kMaxJobs];
 };
 
-// Split-sum owners of a plan: its sorted distinct members (see split_owner).
+// Split-sum owners of a plan: its sorted distinct members (see split_owner_index).
 struct DevOwners {
     int32_t n;
     int16_t rank[kMaxLeaves];
@@ -1486,17 +1486,19 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
 //
 // A group whose members all contributed fresh W' (every stamp == version)
 // and that spans GPUs is summed split: tile t is reduced only by
-// split_owner(t) (same butterfly order, so the bits are unchanged),
+// its owner (split_owner_index; same butterfly order, so the bits are unchanged),
 // which publishes the reduced tile; every other member copies that one tile
 // instead of all S leaves. NVLink ingress per GPU drops from (S-1)·N to
 // about 2(S-1)/S·N. Groups with a stale member are summed by the pull.
 //
-// Warps: 0-7 producers (as in wagma_nvl_kernel); stream A (tiles this GPU
-// reduces itself, and every tile of pulled groups): warp 8 puller, warps
-// 9-16 reducers (sum, publish owned reduced tiles, write W_{t+1}); stream B
-// (tiles reduced by an owner on another GPU): warp 17 puller (waits for the
-// owner's reduced-tile flag, one TMA copy per tile), warps 18-21 finishers.
-// Stream A never waits on stream B, so no cross-GPU wait cycle exists.
+// Warps (R = red_warps, 4 or 8 per launch): 0-7 producers (as in
+// wagma_nvl_kernel); stream A (tiles this GPU reduces itself, and every tile
+// of pulled groups): warp 8 puller, warps 9..8+R reducers (sum, store owned
+// reduced tiles, write W_{t+1}); stream B (tiles reduced by an owner on
+// another GPU): warp 9+R puller (waits for the owner's reduced-tile flag, one
+// TMA copy per tile), warps 10+R..21 finishers; warp 22 publisher (fence +
+// flags for runs of owned reduced tiles). Stream A never waits on stream B,
+// so no cross-GPU wait cycle exists.
 // ---------------------------------------------------------------------------
 
 constexpr int kSplitThreads = 23 * 32;  // + 1 publisher warp (reduced-tile fences and flags)
@@ -1516,10 +1518,11 @@ constexpr int kSplitThreads = 23 * 32;  // + 1 publisher warp (reduced-tile fenc
 constexpr int kRoleWarps = 12;
 
 // Owner of a tile of a split sum: rotates along each CTA's tile sequence so
-// every CTA reduces 1/n_owners of its tiles (tile t is the (t / grid)-th tile
-// of CTA t % grid; the grid is identical on every GPU).
-__device__ __forceinline__ int split_owner(const LaunchParams& p, int pl, int64_t tile) {
-    return p.owners[pl].rank[(tile / gridDim.x) % p.owners[pl].n];
+// every CTA reduces 1/n_owners of its tiles. kc is the CTA-local index of
+// the tile (tile = blockIdx.x + kc * grid; the grid is identical on every
+// GPU), so no division by the grid is needed.
+__device__ __forceinline__ int split_owner_index(const LaunchParams& p, int pl, int kc) {
+    return kc % p.owners[pl].n;
 }
 
 template <typename T>
@@ -1628,7 +1631,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     auto masks = [&](int kc, unsigned& ma, unsigned& mb) {
         ma = mb = 0;
         for (int pl = 0; pl < NP; ++pl) {
-            const bool remote_owner = plan_split[pl] && s_owner_remote[pl][kc % p.owners[pl].n];
+            const bool remote_owner = plan_split[pl] && s_owner_remote[pl][split_owner_index(p, pl, kc)];
             (remote_owner ? mb : ma) |= 1u << pl;
         }
     };
@@ -1863,7 +1866,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 };
                 const V acc = tree_sum<T>(fetch, P_.log_leaves);
                 if (plan_split[pl]) {  // this GPU owns the tile: publish the reduced tile
-                    __stcg(reinterpret_cast<V*>(s_red_base[pl][kc % p.owners[pl].n] + idx), acc);
+                    __stcg(reinterpret_cast<V*>(s_red_base[pl][split_owner_index(p, pl, kc)] + idx), acc);
                     owned = true;
                 }
                 auto own_wp = [&](int j) -> V {
@@ -1953,7 +1956,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             if (e < nb * NP && (btB_mask[e / NP] >> (e % NP) & 1)) {
                 const int pl = e % NP;
                 want = p.versions[p.plans[pl].vidx].version;
-                fp = s_red_flag[pl][btB_kc[e / NP] % p.owners[pl].n] + btB_tile[e / NP];
+                fp = s_red_flag[pl][split_owner_index(p, pl, btB_kc[e / NP])] + btB_tile[e / NP];
                 x = ld_relaxed_sys(fp);
             }
             int rc = 0;
@@ -2000,7 +2003,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 }
                 __syncwarp();
                 if (lane < NP && (mb >> lane & 1)) {
-                    const T* src = s_red_base[lane][btB_kc[bb] % p.owners[lane].n] + tile * p.tile_elems;
+                    const T* src = s_red_base[lane][split_owner_index(p, lane, btB_kc[bb])] + tile * p.tile_elems;
                     bulk_g2s(ringB + (size_t(st) * NP + lane) * kThreads, src, tile_bytes, &fullB[st]);
                 }
                 __syncwarp();
@@ -2071,7 +2074,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             for (int e = lane; e < n * NP; e += 32) {
                 const int slot = int((next + e / NP) & (kRedRing - 1)), pl = e % NP;
                 if (pubq_mask[slot] >> pl & 1)
-                    st_relaxed_sys(s_red_flag[pl][pubq_kc[slot] % p.owners[pl].n] + pubq_tile[slot],
+                    st_relaxed_sys(s_red_flag[pl][split_owner_index(p, pl, pubq_kc[slot])] + pubq_tile[slot],
                                    p.versions[p.plans[pl].vidx].version);
             }
             __syncwarp();
