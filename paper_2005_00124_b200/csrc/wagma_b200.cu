@@ -2155,8 +2155,14 @@ struct ReplicaPtrs {
 template <typename T>
 __global__ void replicas_sum_kernel(ReplicaPtrs ptrs, int R, int64_t n, double* sum) {
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        T v[kMaxJobs];  // every replica's load in flight before the adds
+#pragma unroll
+        for (int r = 0; r < kMaxJobs; ++r)
+            if (r < R) v[r] = __ldcs(static_cast<const T*>(ptrs.w[r]) + e);
         double acc = 0.0;
-        for (int r = 0; r < R; ++r) acc += double(static_cast<const T*>(ptrs.w[r])[e]);
+#pragma unroll
+        for (int r = 0; r < kMaxJobs; ++r)
+            if (r < R) acc += double(v[r]);
         sum[e] += acc;
     }
 }
@@ -2166,10 +2172,16 @@ template <typename T>
 __global__ void replicas_spread_kernel(ReplicaPtrs ptrs, int R, int64_t n, const double* mu, double* out) {
     double g = 0.0, dmax = 0.0;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        T v[kMaxJobs];  // every replica's load in flight before the arithmetic
+#pragma unroll
+        for (int r = 0; r < kMaxJobs; ++r)
+            if (r < R) v[r] = __ldcs(static_cast<const T*>(ptrs.w[r]) + e);
         const double m = mu[e];
-        const double w0 = double(static_cast<const T*>(ptrs.w[0])[e]);
-        for (int r = 0; r < R; ++r) {
-            const double w = double(static_cast<const T*>(ptrs.w[r])[e]);
+        const double w0 = double(v[0]);
+#pragma unroll
+        for (int r = 0; r < kMaxJobs; ++r) {
+            if (r >= R) break;
+            const double w = double(v[r]);
             g += (w - m) * (w - m);
             dmax = fmax(dmax, fabs(w - w0));
         }
