@@ -20,7 +20,7 @@ import torch
 
 from .context import DeviceContext
 
-__all__ = ["ReplicaDiagnostics", "replica_diagnostics"]
+__all__ = ["ReplicaDiagnostics", "replica_diagnostics", "gamma_bound", "check_after_sync"]
 
 
 @dataclass
@@ -53,3 +53,18 @@ def replica_diagnostics(ctx: DeviceContext, replicas: Mapping[int, torch.Tensor]
         dist.all_reduce(out[:1], group=process_group)
     gamma = float(out[0].item())
     return ReplicaDiagnostics(mu=mu, gamma=gamma, identical=gamma == 0.0)
+
+
+def gamma_bound(P: int, eta: float, M_hat: float, tau: int) -> float:
+    """Replica-spread bound 16 P eta^2 M^2 tau^2 the potential is checked against (optim.py:213-215)."""
+    return 16.0 * P * eta ** 2 * M_hat ** 2 * tau ** 2
+
+
+def check_after_sync(diag: ReplicaDiagnostics, t: int) -> None:
+    """The recorder's post-sync rule (optim.py:289-293): after a global sync the
+    spread must vanish (relative to |mu|^2), else ProtocolFault."""
+    from .collective import ProtocolFault
+
+    mu_sq = float(torch.dot(diag.mu, diag.mu).item())
+    if diag.gamma > 1e-12 * max(1.0, mu_sq):
+        raise ProtocolFault(f"replica spread {diag.gamma} nonzero after sync at t={t}")

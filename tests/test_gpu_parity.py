@@ -209,7 +209,8 @@ def test_launch_validation(cuda):
 
 def test_replica_diagnostics(cuda):
     """Gamma_t and the post-sync bit-identity check (optim.py:199-210, 289-293)."""
-    from paper_2005_00124_b200.diagnostics import replica_diagnostics
+    from paper_2005_00124_b200.collective import ProtocolFault
+    from paper_2005_00124_b200.diagnostics import check_after_sync, gamma_bound, replica_diagnostics
     P, S, n, tau, T = 4, 2, 3001, 3, 6
     ctx = DeviceContext(P, S, n, tau=tau, timeout_s=5.0)
     cfg = OptimizerConfig(T=T, S=S, tau=tau, eta=EtaSchedule(value=0.1), update_rule="momentum")
@@ -224,4 +225,10 @@ def test_replica_diagnostics(cuda):
         assert np.allclose(d.mu.cpu().numpy(), mu, rtol=0, atol=1e-12)
         assert d.gamma == pytest.approx(float(((W - mu) ** 2).sum()), rel=1e-9)
         assert d.identical == ((t + 1) % tau == 0)  # bit-identical exactly after each global sync
+        if d.identical:
+            check_after_sync(d, t)
+        else:
+            with pytest.raises(ProtocolFault):
+                check_after_sync(d, t)
+    assert gamma_bound(8, 0.1, 2.0, 10) == pytest.approx(16 * 8 * 0.01 * 4 * 100)
     ctx.close()
