@@ -217,7 +217,8 @@ def step_bytes(a, G, gpu_index, t, elem):
     hbm = R * 6 * n
     nvl = 0.0
     sync = (t + 1) % a.tau == 0
-    split_on = os.environ.get("WG_SPLIT", "1") != "0" and G >= 2 and a.P <= 8
+    split_on = os.environ.get("WG_SPLIT", "1") != "0" and G >= 2 and a.P <= 8 and \
+        n >= int(os.environ.get("WG_SPLIT_MIN_BYTES", str(8 << 20)))  # the kernel's split_min_bytes
     groups = [tuple(range(a.P))] if sync else None
     if not sync:
         part = compute_groups(GroupingParams(a.P, a.S, t))

@@ -2251,6 +2251,7 @@ struct wg_ctx {
     int use_nvl;
     int use_split;
     int split_span;
+    int64_t split_min_bytes;  // split sums only for replicas at least this large
     int occ_nvl[2];
     int occ_split[2];
 };
@@ -2298,6 +2299,11 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     if (const char* sp = getenv("WG_SPLIT")) ctx->use_split = atoi(sp);
     ctx->split_span = 2;  // the same on every process of a job (environment knob for experiments)
     if (const char* ss = getenv("WG_SPLIT_SPAN")) ctx->split_span = std::max(2, atoi(ss));
+    // below ~8 MiB per replica the extra owner -> member hop of a split sum
+    // costs more than the NVLink bytes it saves (measured: 4 GPUs S=4, 1 MiB
+    // pull 0.047 vs split 0.059 ms, 4 MiB 0.069 vs 0.080, 16 MiB 0.130 vs 0.125)
+    ctx->split_min_bytes = int64_t(8) << 20;
+    if (const char* sm = getenv("WG_SPLIT_MIN_BYTES")) ctx->split_min_bytes = std::max<long long>(0, atoll(sm));
     ctx->fence_scope = 1;  // GPU scope for per-tile flags (see publish_tile)
     if (const char* fs = getenv("WG_FENCE_SCOPE")) {
         if (!strcmp(fs, "sys")) ctx->fence_scope = 0;
@@ -2722,7 +2728,8 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         wide = wide || (__builtin_popcount(gpus) >= ctx->split_span && p.owners[k].n == p.plans[k].n_leaves &&
                         split_pays(p.owners[k].n, __builtin_popcount(gpus)));
     }
-    if (p.need_fence && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= ctx->split_span && wide) {
+    if (p.need_fence && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= ctx->split_span && wide &&
+        c.n * int64_t(ctx->esize) >= ctx->split_min_bytes) {
         // split sums: every GPU of a job makes this same choice (it depends on
         // P and the process-wide knob only), so owners always publish the
         // reduced tiles their peers wait for

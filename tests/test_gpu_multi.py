@@ -31,7 +31,9 @@ def _run(tmp_path, G, port, **kw):
             os.path.join(ROOT, "tests", "multigpu_worker.py"), "--out", str(tmp_path)]
     for k, v in kw.items():
         args += [f"--{k.replace('_', '-')}", str(v)]
-    res = subprocess.run(args, capture_output=True, text=True, timeout=600)
+    # small test vectors: keep the split-sum kernel in play (it is off below 8 MiB by default)
+    env = dict(os.environ, WG_SPLIT_MIN_BYTES="0")
+    res = subprocess.run(args, capture_output=True, text=True, timeout=600, env=env)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     return [dict(np.load(os.path.join(tmp_path, f"rank{r}.npz"))) for r in range(G)]
 
