@@ -27,3 +27,33 @@ def test_reference_arm_json_line():
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
     assert line["e2e"] == {"value": line["value"], "unit": "iters/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
+
+
+def _bench_module():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def test_algorithmic_bytes_per_launch():
+    """Roofline numerators: pull leaves, split sums, one GPU."""
+    import types
+
+    b = _bench_module()
+    n = 25_559_081
+    N = 4.0 * n  # bytes per fp32 replica
+    a = types.SimpleNamespace(P=8, S=8, tau=10, n=n)
+    hbm, nvl = b.step_bytes(a, 1, 0, 0, 4)  # all 8 ranks local: 6 streams each, no NVLink
+    assert nvl == 0 and hbm == 8 * 6 * N
+    hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)  # split over 4 GPUs: f = 2/8 -> f*6 + 3/4 = 2.25 N
+    assert nvl == 2.25 * N
+    hbm, nvl = b.step_bytes(a, 8, 0, 0, 4)  # one rank per GPU: 1/8*7 + 7/8 = 1.75 N
+    assert nvl == 1.75 * N
+    a = types.SimpleNamespace(P=4, S=2, tau=10, n=n)
+    hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)  # S=2 pairs across GPUs: split does not pay, pull 1 leaf
+    assert nvl == N and hbm == 6 * N + N
+    a = types.SimpleNamespace(P=4, S=4, tau=10, n=262_144)  # 1 MiB: below the split threshold
+    hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)
+    assert nvl == 3 * 4.0 * 262_144
