@@ -16,6 +16,7 @@
  *   WG_EPROTO    -> collective.ProtocolFault (torn read, recycled descriptor, ...)
  *   WG_ETIMEOUT  -> collective.ProtocolFault (device watchdog: a peer never published)
  *   WG_ECUDA     -> RuntimeError (CUDA runtime failure)
+ *   WG_EDIVERGE  -> optim.DivergenceError (non-finite gradient, optim.py:174-175)
  */
 #ifndef WAGMA_B200_H
 #define WAGMA_B200_H
@@ -35,6 +36,7 @@ extern "C" {
 #define WG_ETIMEOUT 5
 #define WG_ECUDA 6
 #define WG_ENOMEM 7
+#define WG_EDIVERGE 8 /* non-finite W' produced (gradient or replica); optim.DivergenceError */
 
 #define WG_RULE_EXAMPLE 0 /* topology.MASK_RULE_EXAMPLE ("example") */
 #define WG_RULE_LITERAL 1 /* topology.MASK_RULE_LITERAL ("literal") */
@@ -181,6 +183,12 @@ int wg_query_version(wg_ctx* ctx, int64_t version, int64_t* stamps, int* locked)
 
 /* Latched device error word (0 = none) and a one-line description. */
 int wg_ctx_error(wg_ctx* ctx, int* code, int64_t* info);
+
+/* Same error word, read from its host-mapped mirror without synchronising
+ * any stream (errors latched by kernels that are still running may not be
+ * visible yet). Lets a host loop raise DivergenceError one step later
+ * instead of forcing a device round trip every iteration. */
+int wg_ctx_error_async(wg_ctx* ctx, int* code, int64_t* info);
 int wg_ctx_clear_error(wg_ctx* ctx);
 
 /* Straggler injection (StragglerPolicy + compute_delay, netsim.py:64-117):

@@ -12,7 +12,7 @@ import os
 
 from . import _build
 
-WG_OK, WG_EINVAL, WG_EVERSION, WG_ESTALE, WG_EPROTO, WG_ETIMEOUT, WG_ECUDA, WG_ENOMEM = range(8)
+WG_OK, WG_EINVAL, WG_EVERSION, WG_ESTALE, WG_EPROTO, WG_ETIMEOUT, WG_ECUDA, WG_ENOMEM, WG_EDIVERGE = range(9)
 WG_RULE_EXAMPLE, WG_RULE_LITERAL = 0, 1
 WG_F32, WG_F64 = 0, 1
 WG_JOB_STEP, WG_JOB_SYNC_STEP, WG_JOB_LOCAL_STEP, WG_JOB_GROUP_SUM, WG_JOB_SYNC_SUM = range(5)
@@ -76,6 +76,7 @@ SIGNATURES = {
     "wg_launch_status": (_I, [_VP, _I, ctypes.POINTER(WgJobStatus)]),
     "wg_query_version": (_I, [_VP, _I64, _PI64, _PI]),
     "wg_ctx_error": (_I, [_VP, _PI, _PI64]),
+    "wg_ctx_error_async": (_I, [_VP, _PI, _PI64]),
     "wg_ctx_clear_error": (_I, [_VP]),
     "wg_delay": (_I, [_VP, _I64, _VP]),
     "wg_replicas_sum": (_I, [_VP, ctypes.POINTER(_VP), _I, _VP, _VP]),

@@ -24,7 +24,7 @@ import torch
 from . import _lib
 from .topology import InvalidParamsError
 
-__all__ = ["DeviceContext", "Job", "JobStatus", "DeviceProtocolFault"]
+__all__ = ["DeviceContext", "Job", "JobStatus", "DeviceProtocolFault", "DivergenceError"]
 
 
 class DeviceProtocolFault(RuntimeError):
@@ -34,6 +34,19 @@ class DeviceProtocolFault(RuntimeError):
         super().__init__(msg)
         self.code = code
         self.info = info
+
+
+class DivergenceError(RuntimeError):
+    """Non-finite gradient or loss encountered during training (optim.py:81-82).
+
+    Raised when a fused launch latched WG_EDIVERGE: a rank produced a
+    non-finite W' (the reference raises on a non-finite gradient before the
+    update, optim.py:174-175). ``rank`` is the first diverging rank.
+    """
+
+    def __init__(self, msg: str, rank: int = -1):
+        super().__init__(msg)
+        self.rank = rank
 
 
 def _dtype_code(dtype: torch.dtype) -> int:
@@ -106,6 +119,11 @@ class DeviceContext:
         self.P, self.S, self.n = int(P), int(S), int(n)
         self.dtype = dtype
         self.tau = tau
+        # the reference builds every endpoint with staleness_bound=opt.tau
+        # (optim.py:386): default to tau, so over-stale contributions fault
+        if staleness_bound is None:
+            staleness_bound = tau
+        self.staleness_bound = int(staleness_bound) if staleness_bound else None
         self.mask_rule = mask_rule
         self.activation_enabled = bool(activation_enabled)
         self.n_gpus, self.gpu_index = int(n_gpus), int(gpu_index)
@@ -160,12 +178,28 @@ class DeviceContext:
         self._raise(self.lib.wg_ctx_error(self._h, ctypes.byref(code), ctypes.byref(info)), "wg_ctx_error")
         return code.value, info.value
 
+    def _fault(self, code: int, info: int) -> Exception:
+        if code == _lib.WG_EDIVERGE:
+            return DivergenceError(f"non-finite gradient or replica at rank {info} (device)", rank=info)
+        return DeviceProtocolFault(code, info, f"device error {code} "
+                                   f"({self.lib.wg_strerror(code).decode()}), info={info}")
+
     def check(self) -> None:
-        """Raise DeviceProtocolFault if the device latched an error."""
+        """Raise DeviceProtocolFault / DivergenceError if the device latched an error."""
         code, info = self.error()
         if code:
-            raise DeviceProtocolFault(code, info, f"device error {code} "
-                                      f"({self.lib.wg_strerror(code).decode()}), info={info}")
+            raise self._fault(code, info)
+
+    def check_async(self) -> None:
+        """Like check(), from the host-mapped error mirror: no stream synchronisation.
+
+        Sees the errors of finished launches (and possibly of running ones).
+        """
+        code, info = ctypes.c_int(), ctypes.c_int64()
+        self._raise(self.lib.wg_ctx_error_async(self._h, ctypes.byref(code), ctypes.byref(info)),
+                    "wg_ctx_error_async")
+        if code.value:
+            raise self._fault(code.value, info.value)
 
     def clear_error(self) -> None:
         self._raise(self.lib.wg_ctx_clear_error(self._h), "wg_ctx_clear_error")
@@ -239,7 +273,13 @@ class DeviceContext:
             for name in ("g", "fresh"):  # read-only inputs: realign if needed
                 t = getattr(j, name)
                 if t is not None and t.data_ptr() % 16:
-                    t = t.clone()
+                    # copy on the launch stream (after the caller's pending work)
+                    cur = torch.cuda.current_stream(self.torch_device)
+                    ls = stream if stream is not None else cur
+                    if ls is not cur:
+                        ls.wait_stream(cur)
+                    with torch.cuda.stream(ls):
+                        t = t.clone()
                     keep.append(t)
                     setattr(j, name, t)
             for name in ("W", "m", "g", "fresh", "acc_out"):

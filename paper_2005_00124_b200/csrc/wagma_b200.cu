@@ -149,6 +149,8 @@ struct LaunchParams {
     int32_t split_stages; // reduced-tile ring stages of the split kernel
     int32_t split_span;   // minimum GPUs a group must span to be summed split
     int32_t red_warps;    // split kernel: stream-A reducer warps (4 or 8 of the 12 shared with stream B)
+    int32_t loc_stages;   // single-GPU TMA kernel: input-ring stages
+    int64_t* err_host;    // host-mapped mirror of the error word (wg_ctx_error_async)
 };
 
 // ---------------------------------------------------------------------------
@@ -226,6 +228,16 @@ __device__ __forceinline__ double2 vscale(double s, double2 a) {
 }
 __device__ __forceinline__ double2 vdiv(double2 a, double d) {
     return make_double2(__ddiv_rn(a.x, d), __ddiv_rn(a.y, d));
+}
+// Non-finite component (NaN or +-Inf): the reference raises DivergenceError
+// on a non-finite gradient (optim.py:174-175); a non-finite g, m or W makes
+// W' non-finite, so the produced W' is what is checked.
+__device__ __forceinline__ bool nonfinite(float4 v) {
+    return !(fabsf(v.x) <= 3.402823466e38f && fabsf(v.y) <= 3.402823466e38f && fabsf(v.z) <= 3.402823466e38f &&
+             fabsf(v.w) <= 3.402823466e38f);
+}
+__device__ __forceinline__ bool nonfinite(double2 v) {
+    return !(fabs(v.x) <= 1.7976931348623157e308 && fabs(v.y) <= 1.7976931348623157e308);
 }
 
 // Caller-owned vectors (W, m, g, fresh, acc_out) have exactly n elements:
@@ -309,8 +321,13 @@ __device__ __forceinline__ int64_t* err_ptr(const LaunchParams& p) {
 
 __device__ __noinline__ void raise_error(const LaunchParams& p, int code, int64_t info) {
     int64_t* e = err_ptr(p);
-    if (atomicCAS(reinterpret_cast<unsigned long long*>(e), 0ull, (unsigned long long)code) == 0ull)
+    if (atomicCAS(reinterpret_cast<unsigned long long*>(e), 0ull, (unsigned long long)code) == 0ull) {
         e[1] = info;
+        if (p.err_host) {  // host-mapped mirror: info first, then the code
+            st_relaxed_sys(p.err_host + 1, info);
+            st_release_sys(p.err_host, code);
+        }
+    }
     __threadfence_system();
 }
 __device__ __forceinline__ bool aborted(const LaunchParams& p) {
@@ -603,9 +620,9 @@ __device__ __forceinline__ void init_ring_slots(const LaunchParams& p, T** ring_
 }
 
 // Local step of one item + send-ring install + stage (optim.py:176-183,
-// collective.py:95-101).
+// collective.py:95-101). Returns true if the produced W' is non-finite.
 template <typename T, bool STAGE = true>
-__device__ __forceinline__ void compute_item(const LaunchParams& p, int64_t tile, int j,
+__device__ __forceinline__ bool compute_item(const LaunchParams& p, int64_t tile, int j,
                                              const typename Tr<T>::V* slot, typename Tr<T>::V* stage,
                                              T* const* ring_slot) {
     using V = typename Tr<T>::V;
@@ -614,6 +631,7 @@ __device__ __forceinline__ void compute_item(const LaunchParams& p, int64_t tile
     const int64_t idx = tile * p.tile_elems + int64_t(tid) * E;
     const DevJob& jb = p.jobs[j];
     V wp;
+    bool bad = false;
     if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
         wp = slot[tid];
     } else {
@@ -628,15 +646,24 @@ __device__ __forceinline__ void compute_item(const LaunchParams& p, int64_t tile
         } else {
             wp = vsub(w, vscale(eta, g));  // W' = W - eta*g (optim.py:181-183)
         }
+        bad = nonfinite(wp);  // zero-filled past n: the ragged end stays finite
         if (jb.kind == WG_JOB_LOCAL_STEP) {
             st_stream<T>(static_cast<T*>(jb.W), idx, p.n, wp);
-            return;
+            return bad;
         }
     }
     // SendBuffer.install: W' written once into the send ring, and staged
     T* const rs = ring_slot ? ring_slot[j] : ring_ptr<T>(p, jb.rank, slot_of(p, jb.version));
     __stcg(reinterpret_cast<V*>(rs + idx), wp);
     if (STAGE) stage[j * kThreads + tid] = wp;
+    return bad;
+}
+
+// Latch DivergenceError (optim.py:174-175) for the jobs whose produced W'
+// was non-finite in any thread of the warp: `bad` is a per-thread job mask.
+__device__ __forceinline__ void report_divergence(const LaunchParams& p, unsigned bad) {
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && (threadIdx.x & 31) == 0) raise_error(p, WG_EDIVERGE, p.jobs[__ffs(bad) - 1].rank);
 }
 
 // Multi-GPU kernel: register-pipelined produce (the next job's loads in
@@ -670,7 +697,7 @@ __device__ __forceinline__ void load_job(const LaunchParams& p, const DevJob& jb
 
 template <typename T>
 __device__ __forceinline__ void produce_tile_regs(const LaunchParams& p, int64_t tile, typename Tr<T>::V* stage,
-                                                  T* const* ring_slot) {
+                                                  T* const* ring_slot, unsigned& bad) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
     constexpr int U = kVecPerThread;
@@ -705,6 +732,8 @@ __device__ __forceinline__ void produce_tile_regs(const LaunchParams& p, int64_t
 #pragma unroll
                 for (int k = 0; k < U; ++k) wp[k] = vsub(cw[k], vscale(eta, cg[k]));
             }
+#pragma unroll
+            for (int k = 0; k < U; ++k) bad |= unsigned(nonfinite(wp[k])) << j;
             if (jb.kind == WG_JOB_LOCAL_STEP) {
                 T* W = static_cast<T*>(jb.W);
 #pragma unroll
@@ -924,6 +953,7 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
     }
     bool resolved = false;
     unsigned my_tiles = 0;
+    unsigned bad = 0;  // jobs whose W' was non-finite in this thread
     if constexpr (AHEAD) {
         V* stages[2] = {stage, stage + size_t(p.n_jobs) * kVecPerThread * kThreads};
         const bool prof = p.prof != nullptr && threadIdx.x == 0;
@@ -939,7 +969,7 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
         int64_t tile = blockIdx.x;
         int buf = 0;
         if (tile < p.n_tiles) {
-            produce_tile_regs<T>(p, tile, stages[0], s_ring);
+            produce_tile_regs<T>(p, tile, stages[0], s_ring, bad);
             lap(0);
             publish_tile(p, tile);
             lap(1);
@@ -948,7 +978,7 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
         while (tile < p.n_tiles) {
             const int64_t next = tile + gridDim.x;
             if (next < p.n_tiles) {
-                produce_tile_regs<T>(p, next, stages[buf ^ 1], s_ring);
+                produce_tile_regs<T>(p, next, stages[buf ^ 1], s_ring, bad);
                 lap(0);
                 publish_tile(p, next);
                 lap(1);
@@ -992,7 +1022,7 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
             for (int j = 0; j < J; ++j) {
                 cp_async_wait<kDepth - 1>();
                 V* slot = ring + rs * 3 * kThreads;
-                compute_item<T>(p, tile, j, slot, st, WG_STEP_SRING ? s_ring : nullptr);
+                bad |= unsigned(compute_item<T>(p, tile, j, slot, st, WG_STEP_SRING ? s_ring : nullptr)) << j;
                 if (ik < my_ntiles) issue_item<T>(p, int64_t(blockIdx.x) + ik * gridDim.x, ij, slot);
                 cp_async_commit();
                 if (++ij == J) ij = 0, ++ik;
@@ -1012,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
             for (int j = 0; j < J; ++j, ++i) {
                 cp_async_wait<kDepth - 1>();
                 V* slot = ring + (i % kDepth) * 3 * kThreads;
-                compute_item<T>(p, tile, j, slot, st, WG_STEP_SRING ? s_ring : nullptr);
+                bad |= unsigned(compute_item<T>(p, tile, j, slot, st, WG_STEP_SRING ? s_ring : nullptr)) << j;
                 const int64_t nx = i + kDepth;
                 if (nx < n_items)
                     issue_item<T>(p, int64_t(blockIdx.x) + (nx / J) * int64_t(gridDim.x), int(nx % J), slot);
@@ -1028,6 +1058,7 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
         }
         cp_async_wait<0>();
     }
+    report_divergence(p, bad);
     publish_slots(p, sm.abort ? 0u : my_tiles);
     if (blockIdx.x == 0) {
         if (!resolved && !sm.abort) resolved = resolve_sources<T>(p, sm);
@@ -1146,6 +1177,246 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// single-GPU kernel: TMA producer warp, control warp, consumer warps
+//
+// All ranks of the launch live on this GPU, so nobody outside a CTA waits on
+// its tiles and the step is a pure HBM stream: per chunk (kLocTiles tiles)
+// and job, read W, g, m and write m, W' (send ring) and W_{t+1}.
+//  - warp 0 (one elected lane) streams the inputs of every (chunk, job) item
+//    with cp.async.bulk (TMA bulk copies, UBLKCP) into a ring of NS stages
+//    guarded by mbarriers (full: bytes landed; empty: consumed), so the
+//    bytes in flight per SM are set by the ring, not by registers;
+//  - warp 1 runs the activation protocol (CTA 0) and resolves every plan's
+//    leaves while the first items are being loaded and computed;
+//  - the consumer warps compute the local step of each item from shared
+//    memory, store m and the W' send-ring slot, keep W' in a thread-private
+//    shared-memory stage, then sum each plan in the butterfly order and write
+//    W_{t+1} (timely acc/S, late (acc + W')/(S+1), sync total/P).
+// Every index is advanced incrementally (no 64-bit division per item).
+// ---------------------------------------------------------------------------
+
+#ifndef WG_LOC_TILES
+#define WG_LOC_TILES 2
+#endif
+#ifndef WG_LOC_CONSUMER_WARPS
+#define WG_LOC_CONSUMER_WARPS 8
+#endif
+constexpr int kLocTiles = WG_LOC_TILES;                    // tiles per chunk (per item)
+constexpr int kLocConsumers = WG_LOC_CONSUMER_WARPS * 32;  // consumer threads
+constexpr int kLocThreads = kLocConsumers + 64;            // + producer warp + control warp
+constexpr int kLocChunkVecs = kLocTiles * kThreads;        // 16-byte vectors per row of a stage
+constexpr int kLocVPT = kLocChunkVecs / kLocConsumers;     // vectors per consumer thread per item
+constexpr int kLocMaxStages = 16;
+static_assert(kLocChunkVecs % kLocConsumers == 0, "a chunk row must split evenly over the consumers");
+
+template <typename T>
+__global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __grid_constant__ LaunchParams p) {
+    using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
+    extern __shared__ __align__(128) unsigned char dyn_smem[];
+    __shared__ SmemCtl sm;
+    __shared__ T* s_ring[kMaxJobs];
+    __shared__ __align__(8) uint64_t full[kLocMaxStages];
+    __shared__ __align__(8) uint64_t empty[kLocMaxStages];
+    __shared__ volatile int ready;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int J = p.n_jobs, NS = p.loc_stages;
+    const int64_t chunk_elems = int64_t(kLocChunkVecs) * E;
+    const int64_t n_chunks = (p.n_tiles + kLocTiles - 1) / kLocTiles;
+    V* rows = reinterpret_cast<V*>(dyn_smem);               // [NS][3][kLocChunkVecs]: W, g, m of an item
+    V* wst = rows + size_t(NS) * 3 * kLocChunkVecs;         // [J][kLocChunkVecs]: W' of every job
+    if (tid == 0) {
+        sm.abort = 0;
+        ready = 0;
+        for (int st = 0; st < NS; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], kLocConsumers / 32);
+        }
+    }
+    if (tid < kMaxVersions) sm.activator[tid] = 0;
+    init_ring_slots<T>(p, s_ring);
+    __syncthreads();
+
+    if (warp == 0) {
+        // ---------------- producer: TMA bulk loads of every item ----------------
+        if (lane == 0) {
+            constexpr unsigned chunk_bytes = unsigned(kLocChunkVecs) * 16u;
+            int st = 0;
+            unsigned ph = 0;
+            int64_t k = 0;
+            bool ok = true;
+            for (int64_t c = blockIdx.x; c < n_chunks && ok; c += gridDim.x) {
+                const int64_t e0 = c * chunk_elems;
+                // caller vectors hold exactly n elements: whole 16-byte vectors by
+                // TMA, the ragged end is read by the consumers from global memory
+                const int64_t rem = (p.n - e0) * int64_t(sizeof(T));
+                const unsigned bytes = rem >= chunk_bytes ? chunk_bytes : (rem > 0 ? unsigned(rem) & ~15u : 0u);
+                for (int j = 0; j < J; ++j, ++k) {
+                    if (k >= NS && !mbar_wait(p, &empty[st], ph ^ 1u)) {
+                        ok = false;
+                        break;
+                    }
+                    const DevJob& jb = p.jobs[j];
+                    V* dst = rows + size_t(st) * 3 * kLocChunkVecs;
+                    if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
+                        mbar_arrive_expect_tx(&full[st], bytes);
+                        if (bytes) bulk_g2s(dst, static_cast<const T*>(jb.fresh) + e0, bytes, &full[st]);
+                    } else {
+                        const bool mom = jb.update_rule == WG_UPDATE_MOMENTUM;
+                        mbar_arrive_expect_tx(&full[st], (mom ? 3u : 2u) * bytes);
+                        if (bytes) {
+                            bulk_g2s(dst, static_cast<const T*>(jb.W) + e0, bytes, &full[st]);
+                            bulk_g2s(dst + kLocChunkVecs, static_cast<const T*>(jb.g) + e0, bytes, &full[st]);
+                            if (mom) bulk_g2s(dst + 2 * kLocChunkVecs, static_cast<const T*>(jb.m) + e0, bytes, &full[st]);
+                        }
+                    }
+                    if (++st == NS) st = 0, ph ^= 1u;
+                }
+            }
+            if (!ok) {
+                raise_error(p, WG_ETIMEOUT, k);
+                sm.abort = 1;
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- control: activation + leaf sources ----------------
+        if (blockIdx.x == 0) control_phase(p, sm.activator);
+        bool res = resolve_core<T>(p, sm, lane, 32, [] { __syncwarp(); });
+        // a leaf slot still being filled by an earlier launch (another
+        // stream): wait until its launch completed the slot
+        if (res && lane == 0) {
+            const uint64_t t0 = globaltimer();
+            for (int pl = 0; pl < p.n_plans && res; ++pl)
+                for (int li = 0; li < p.plans[pl].n_leaves && res; ++li) {
+                    if (sm.leaf_src[pl][li] != kSrcPoll) continue;
+                    const int q = p.plans[pl].leaves[li];
+                    const int rc = spin_eq(p, complete_ptr(p, q, sm.leaf_slot[pl][li]),
+                                           sm.stamps[p.plans[pl].vidx][q], t0);
+                    if (rc) {
+                        raise_error(p, rc, q);
+                        sm.abort = 1;
+                        res = false;
+                    }
+                    sm.leaf_src[pl][li] = kSrcReady;
+                }
+        }
+        res = __shfl_sync(0xffffffffu, res, 0);
+        if (lane == 0) {
+            __threadfence_block();
+            ready = res ? 1 : 2;
+        }
+    } else {
+        // ---------------- consumers ----------------
+        const int ct = tid - 64;
+        unsigned bad = 0;
+        int st = 0;
+        unsigned ph = 0;
+        bool ok = true, resolved = false;
+        for (int64_t c = blockIdx.x; c < n_chunks && ok; c += gridDim.x) {
+            const int64_t e0 = c * chunk_elems;
+            for (int j = 0; j < J; ++j) {
+                if (!mbar_wait(p, &full[st], ph)) {
+                    ok = false;
+                    break;
+                }
+                const V* r = rows + size_t(st) * 3 * kLocChunkVecs;
+                const DevJob& jb = p.jobs[j];
+                const bool sum = jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM;
+                const bool mom = jb.update_rule == WG_UPDATE_MOMENTUM;
+                const T eta = T(jb.eta), beta = T(jb.beta);
+                T* const rs = s_ring[j];
+#pragma unroll
+                for (int kv = 0; kv < kLocVPT; ++kv) {
+                    const int v = kv * kLocConsumers + ct;
+                    const int64_t idx = e0 + int64_t(v) * E;
+                    const bool tail = idx + E > p.n;  // ragged end: global loads, zero-filled
+                    V wp;
+                    if (sum) {
+                        wp = tail ? ld_tail(static_cast<const T*>(jb.fresh), idx, p.n) : r[v];
+                    } else {
+                        const V w = tail ? ld_tail(static_cast<const T*>(jb.W), idx, p.n) : r[v];
+                        const V g = tail ? ld_tail(static_cast<const T*>(jb.g), idx, p.n) : r[kLocChunkVecs + v];
+                        if (mom) {
+                            // m = beta*m + g ; W' = W - eta*m  (optim.py:179,183)
+                            const V m0 =
+                                tail ? ld_tail(static_cast<const T*>(jb.m), idx, p.n) : r[2 * kLocChunkVecs + v];
+                            const V mn = vadd(vscale(beta, m0), g);
+                            st_stream<T>(static_cast<T*>(jb.m), idx, p.n, mn);
+                            wp = vsub(w, vscale(eta, mn));
+                        } else {
+                            wp = vsub(w, vscale(eta, g));  // W' = W - eta*g (optim.py:181-183)
+                        }
+                        bad |= unsigned(nonfinite(wp)) << j;
+                        if (jb.kind == WG_JOB_LOCAL_STEP) {
+                            st_stream<T>(static_cast<T*>(jb.W), idx, p.n, wp);
+                            continue;
+                        }
+                    }
+                    // SendBuffer.install (collective.py:95-101): W' once into the ring
+                    if (idx < p.npad) __stcg(reinterpret_cast<V*>(rs + idx), wp);
+                    wst[j * kLocChunkVecs + v] = wp;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+                if (++st == NS) st = 0, ph ^= 1u;
+            }
+            if (!ok) break;
+            if (!resolved) {
+                while (ready == 0) __nanosleep(32);
+                __threadfence_block();
+                if (ready != 1) break;
+                resolved = true;
+            }
+            // group sums in the butterfly order + the averaging rule
+            for (int pl = 0; pl < p.n_plans; ++pl) {
+                const DevPlan& P_ = p.plans[pl];
+#pragma unroll
+                for (int kv = 0; kv < kLocVPT; ++kv) {
+                    const int v = kv * kLocConsumers + ct;
+                    const int64_t idx = e0 + int64_t(v) * E;
+                    if (idx >= p.npad) continue;
+                    auto fetch = [&](int leaf) -> V {
+                        const int src = sm.leaf_src[pl][leaf];
+                        if (src >= 0) return wst[src * kLocChunkVecs + v];
+                        // an older send slot (stale member): L2 / HBM
+                        return __ldcg(reinterpret_cast<const V*>(
+                            ring_ptr<T>(p, P_.leaves[leaf], sm.leaf_slot[pl][leaf]) + idx));
+                    };
+                    finish_members<T>(p, sm, P_, tree_sum<T>(fetch, P_.log_leaves), idx,
+                                      [&](int j) { return wst[j * kLocChunkVecs + v]; });
+                }
+            }
+        }
+        if (!ok) {
+            if (lane == 0) raise_error(p, WG_ETIMEOUT, blockIdx.x);
+            sm.abort = 1;
+        }
+        report_divergence(p, bad);
+    }
+    unsigned my_tiles = 0;
+    for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x)
+        my_tiles += unsigned(p.n_tiles - c * kLocTiles < kLocTiles ? p.n_tiles - c * kLocTiles : kLocTiles);
+    __syncthreads();
+    if (ready != 1) sm.abort = 1;
+    publish_slots(p, sm.abort ? 0u : my_tiles);
+    if (blockIdx.x == 0) {
+        __syncthreads();
+        const bool res = ready == 1;
+        if (tid < p.n_jobs) {
+            const DevJob& jb = p.jobs[tid];
+            wg_job_status stt;
+            stt.version = jb.version;
+            stt.contrib_stamp = (jb.kind == WG_JOB_LOCAL_STEP || !res) ? jb.version : sm.stamps[jb.vidx][jb.rank];
+            stt.timely = stt.contrib_stamp == jb.version;
+            stt.root = activation_root(p, jb, res);
+            stt.activator = jb.vidx >= 0 && sm.activator[jb.vidx] && stt.root == jb.rank;
+            stt.error = int32_t(ld_relaxed_sys(err_ptr(p)));
+            p.status[tid] = stt;
+        }
+    }
+}
+
 // Producer warps of the multi-GPU kernels (warps 0..7): local step of every
 // job for every tile of this CTA, send-ring install, and the tiles'
 // readiness flags published in chunks of kPubChunk by the last warp to
@@ -1154,7 +1425,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 template <typename T, int kNvlDepth>
 __device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename Tr<T>::V* ring, int64_t my_ntiles,
                                                 unsigned* pub_count, T* const* ring_slot,
-                                                int64_t* const* flag_base) {
+                                                int64_t* const* flag_base, unsigned& bad) {
     using V = typename Tr<T>::V;
     const int lane = threadIdx.x & 31;
     const int J = p.n_jobs;
@@ -1174,7 +1445,7 @@ __device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename 
         for (int j = 0; j < J; ++j) {
             cp_async_wait<kNvlDepth - 1>();
             V* slot = ring + rs * 3 * kThreads;
-            compute_item<T, false>(p, tile, j, slot, nullptr, ring_slot);
+            bad |= unsigned(compute_item<T, false>(p, tile, j, slot, nullptr, ring_slot)) << j;
             if (ik < my_ntiles) issue_item<T>(p, int64_t(blockIdx.x) + ik * gridDim.x, ij, slot);
             cp_async_commit();
             if (++ij == J) ij = 0, ++ik;
@@ -1289,7 +1560,9 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     if (warp < kWarps) {
         // ---------------- producers ----------------
         const long long pc0 = clock64();
-        my_tiles = nvl_produce<T, kNvlDepth>(p, ring, my_ntiles, pub_count, s_ring, s_flag0);
+        unsigned bad = 0;
+        my_tiles = nvl_produce<T, kNvlDepth>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad);
+        report_divergence(p, bad);
         if (p.prof && tid == 0) p.prof[blockIdx.x * 8 + 0] = clock64() - pc0;
     } else if (warp == 2 * kWarps) {
         // ---------------- puller ----------------
@@ -1648,7 +1921,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         if (p.prof) p.prof[blockIdx.x * 16 + slot] = v;
     };
     if (warp < kWarps) {
-        my_tiles = nvl_produce<T, kSplitDepth>(p, ring, my_ntiles, pub_count, s_ring, s_flag0);
+        unsigned bad = 0;
+        my_tiles = nvl_produce<T, kSplitDepth>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad);
+        report_divergence(p, bad);
         if (tid == 0) prof_set(0, clock64() - t_start);
     } else if (warp == kWarps) {
         // ---------------- stream A puller ----------------
@@ -2224,6 +2499,11 @@ struct Blob {
     uint64_t magic;
     int32_t gpu_index, P, R, D, Dv, dtype;
     int64_t n, arena_bytes;
+    // process-wide kernel choices that every GPU of a job must share: which
+    // multi-GPU kernel runs (only the split kernel publishes reduced tiles),
+    // its tile ownership (grid = SMs x occupancy) and the flag fence scope
+    int32_t use_nvl, use_split, split_span, fence_scope, sms, occ_split, occ_nvl, pad;
+    int64_t split_min_bytes;
     cudaIpcMemHandle_t handle;
 };
 constexpr uint64_t kBlobMagic = 0x57474d4142323030ull;  // "WGMAB200"
@@ -2254,6 +2534,10 @@ struct wg_ctx {
     int64_t split_min_bytes;  // split sums only for replicas at least this large
     int occ_nvl[2];
     int occ_split[2];
+    int use_loc;              // single-GPU launches: TMA kernel (else the cp.async kernel)
+    int loc_dyn_max[2];       // dynamic shared memory available to wagma_local_kernel<T>
+    int64_t* err_host;        // host-mapped mirror of the error word
+    int64_t* err_host_dev;
 };
 
 extern "C" {
@@ -2268,6 +2552,7 @@ const char* wg_strerror(int code) {
         case WG_ETIMEOUT: return "device watchdog timeout (peer never published)";
         case WG_ECUDA: return "CUDA runtime error";
         case WG_ENOMEM: return "out of memory";
+        case WG_EDIVERGE: return "non-finite gradient or replica (divergence)";
         default: return "unknown error";
     }
 }
@@ -2304,6 +2589,8 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     // pull 0.047 vs split 0.059 ms, 4 MiB 0.069 vs 0.080, 16 MiB 0.130 vs 0.125)
     ctx->split_min_bytes = int64_t(8) << 20;
     if (const char* sm = getenv("WG_SPLIT_MIN_BYTES")) ctx->split_min_bytes = std::max<long long>(0, atoll(sm));
+    ctx->use_loc = 1;
+    if (const char* lc = getenv("WG_LOC")) ctx->use_loc = atoi(lc);
     ctx->fence_scope = 1;  // GPU scope for per-tile flags (see publish_tile)
     if (const char* fs = getenv("WG_FENCE_SCOPE")) {
         if (!strcmp(fs, "sys")) ctx->fence_scope = 0;
@@ -2382,12 +2669,43 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(wagma_split_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNvlMaxDyn);
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e)); break; }
+        {
+            int optin = 0;
+            e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device);
+            cudaFuncAttributes fa[2];
+            if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa[0], wagma_local_kernel<float>);
+            if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa[1], wagma_local_kernel<double>);
+            for (int di = 0; di < 2 && e == cudaSuccess; ++di) {
+                ctx->loc_dyn_max[di] = optin - int(fa[di].sharedSizeBytes) - 1024;
+                e = cudaFuncSetAttribute(di == 0 ? (const void*)wagma_local_kernel<float> : (const void*)wagma_local_kernel<double>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->loc_dyn_max[di]);
+            }
+            if (e != cudaSuccess) { rc = fail(WG_ECUDA, "local kernel attributes: %s", cudaGetErrorString(e)); break; }
+        }
+        e = cudaHostAlloc(&ctx->err_host, 2 * sizeof(int64_t), cudaHostAllocMapped);
+        if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaHostAlloc: %s", cudaGetErrorString(e)); break; }
+        ctx->err_host[0] = ctx->err_host[1] = 0;
+        e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->err_host_dev), ctx->err_host, 0);
+        if (e != cudaSuccess) { rc = fail(WG_ECUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e)); break; }
         e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, c.device);
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "device attribute: %s", cudaGetErrorString(e)); break; }
+        // multi-GPU grids (tile ownership) are fixed here, so peers can compare them at import
+        for (int di = 0; di < 2 && e == cudaSuccess; ++di) {
+            int o = 0;
+            e = di == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wagma_split_kernel<float>, kSplitThreads, kNvlMaxDyn)
+                        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wagma_split_kernel<double>, kSplitThreads, kNvlMaxDyn);
+            ctx->occ_split[di] = o > 0 ? o : 1;
+            if (e != cudaSuccess) break;
+            e = di == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wagma_nvl_kernel<float>, kNvlThreads, kNvlMaxDyn)
+                        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wagma_nvl_kernel<double>, kNvlThreads, kNvlMaxDyn);
+            ctx->occ_nvl[di] = o > 0 ? o : 1;
+        }
+        if (e != cudaSuccess) { rc = fail(WG_ECUDA, "occupancy: %s", cudaGetErrorString(e)); break; }
     } while (0);
     if (rc != WG_OK) {
         if (ctx->arena) cudaFree(ctx->arena);
         if (ctx->status_host) cudaFreeHost(ctx->status_host);
+        if (ctx->err_host) cudaFreeHost(ctx->err_host);
         delete ctx;
         return rc;
     }
@@ -2405,6 +2723,7 @@ int wg_ctx_destroy(wg_ctx* ctx) {
         if (ctx->opened[g] && ctx->base[g]) cudaIpcCloseMemHandle(ctx->base[g]);
     if (ctx->arena) cudaFree(ctx->arena);
     if (ctx->status_host) cudaFreeHost(ctx->status_host);
+    if (ctx->err_host) cudaFreeHost(ctx->err_host);
     delete ctx;
     return WG_OK;
 }
@@ -2423,6 +2742,14 @@ int wg_ctx_export(wg_ctx* ctx, void* blob, size_t cap, size_t* len) {
     b.dtype = ctx->cfg.dtype;
     b.n = ctx->cfg.n;
     b.arena_bytes = ctx->L.total;
+    b.use_nvl = ctx->use_nvl;
+    b.use_split = ctx->use_split;
+    b.split_span = ctx->split_span;
+    b.fence_scope = ctx->fence_scope;
+    b.sms = ctx->sms;
+    b.occ_split = ctx->occ_split[ctx->cfg.dtype == WG_F32 ? 0 : 1];
+    b.occ_nvl = ctx->occ_nvl[ctx->cfg.dtype == WG_F32 ? 0 : 1];
+    b.split_min_bytes = ctx->split_min_bytes;
     WG_CUDA(cudaSetDevice(ctx->cfg.device));
     WG_CUDA(cudaIpcGetMemHandle(&b.handle, ctx->arena));
     std::memcpy(blob, &b, sizeof(b));
@@ -2441,6 +2768,13 @@ int wg_ctx_import_peer(wg_ctx* ctx, int gpu_index, const void* blob, size_t len)
     if (b.P != ctx->cfg.P || b.R != ctx->R || b.D != ctx->D || b.Dv != ctx->Dv || b.dtype != ctx->cfg.dtype ||
         b.n != ctx->cfg.n || b.arena_bytes != ctx->L.total)
         return fail(WG_EINVAL, "peer %d context geometry differs", gpu_index);
+    const int di = ctx->cfg.dtype == WG_F32 ? 0 : 1;
+    if (b.use_nvl != ctx->use_nvl || b.use_split != ctx->use_split || b.split_span != ctx->split_span ||
+        b.fence_scope != ctx->fence_scope || b.sms != ctx->sms || b.occ_split != ctx->occ_split[di] ||
+        b.occ_nvl != ctx->occ_nvl[di] || b.split_min_bytes != ctx->split_min_bytes)
+        return fail(WG_EINVAL,
+                    "peer %d runs different kernel settings (WG_NVL/WG_SPLIT/WG_SPLIT_SPAN/WG_SPLIT_MIN_BYTES/"
+                    "WG_FENCE_SCOPE or SM count / occupancy differ)", gpu_index);
     if (gpu_index == ctx->cfg.gpu_index) return WG_OK;
     if (ctx->opened[gpu_index]) return WG_OK;
     WG_CUDA(cudaSetDevice(ctx->cfg.device));
@@ -2526,6 +2860,15 @@ static int occupancy(wg_ctx* ctx, int n_stage) {
     return occ;
 }
 
+// Input-ring stages of wagma_local_kernel for a launch of n_jobs jobs (the W'
+// stage takes one chunk row per job); < 2 means the launch does not fit.
+static int local_stages(wg_ctx* ctx, int n_jobs) {
+    const int64_t row = int64_t(kLocChunkVecs) * 16;
+    const int64_t avail = int64_t(ctx->loc_dyn_max[ctx->cfg.dtype == WG_F32 ? 0 : 1]) - int64_t(n_jobs) * row;
+    if (avail < 2 * 3 * row) return 0;
+    return int(std::min<int64_t>(kLocMaxStages, avail / (3 * row)));
+}
+
 int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced_versions,
               const int64_t* forced_stamps, int n_forced, void* stream) {
     if (!ctx || (!jobs && n_jobs)) return fail(WG_EINVAL, "null argument");
@@ -2559,6 +2902,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
     p.prof = ctx->prof;
     p.fence_scope = ctx->fence_scope;
     p.split_span = ctx->split_span;
+    p.err_host = ctx->err_host_dev;
     for (int q = 0; q < kMaxP; ++q) p.job_of_rank[q] = -1;
 
     const size_t align_mask = 15;
@@ -2796,6 +3140,16 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
             wagma_nvl_kernel<float><<<unsigned(g), kNvlThreads, nvl_smem, s>>>(p);
         else
             wagma_nvl_kernel<double><<<unsigned(g), kNvlThreads, nvl_smem, s>>>(p);
+    } else if (!p.need_fence && ctx->use_loc &&
+               (p.loc_stages = local_stages(ctx, n_jobs)) >= 2) {
+        const size_t row = size_t(kLocChunkVecs) * 16;
+        const size_t loc_smem = (size_t(p.loc_stages) * 3 + size_t(n_jobs)) * row;
+        const int64_t n_chunks = (ctx->n_tiles + kLocTiles - 1) / kLocTiles;
+        const int64_t g = std::min<int64_t>(n_chunks, ctx->sms);
+        if (c.dtype == WG_F32)
+            wagma_local_kernel<float><<<unsigned(g), kLocThreads, loc_smem, s>>>(p);
+        else
+            wagma_local_kernel<double><<<unsigned(g), kLocThreads, loc_smem, s>>>(p);
     } else if (c.dtype == WG_F32) {
         if (p.need_fence)
             wagma_step_kernel<float, true><<<unsigned(grid), kThreads, smem, s>>>(p);
@@ -2841,10 +3195,19 @@ int wg_ctx_error(wg_ctx* ctx, int* code, int64_t* info) {
     return WG_OK;
 }
 
+int wg_ctx_error_async(wg_ctx* ctx, int* code, int64_t* info) {
+    if (!ctx || !code) return fail(WG_EINVAL, "null argument");
+    const volatile int64_t* h = ctx->err_host;
+    *code = int(h[0]);
+    if (info) *info = h[1];
+    return WG_OK;
+}
+
 int wg_ctx_clear_error(wg_ctx* ctx) {
     if (!ctx) return fail(WG_EINVAL, "null ctx");
     WG_CUDA(cudaSetDevice(ctx->cfg.device));
     WG_CUDA(cudaMemset(ctx->arena + ctx->L.hdr, 0, 16));
+    ctx->err_host[0] = ctx->err_host[1] = 0;
     return WG_OK;
 }
 

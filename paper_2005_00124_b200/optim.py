@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .context import DeviceContext, Job, JobStatus
+from .context import DeviceContext, DivergenceError, Job, JobStatus
 from .topology import GroupingParams
 
 __all__ = [
@@ -34,10 +34,6 @@ __all__ = [
 
 class ConfigError(ValueError):
     """Invalid run configuration (optim.py:77-78)."""
-
-
-class DivergenceError(RuntimeError):
-    """Non-finite gradient or loss encountered during training (optim.py:81-82)."""
 
 
 @dataclass(frozen=True)
@@ -130,6 +126,11 @@ class GroupAveragingOptimizer:
             raise ConfigError("alpha/beta must match the context's activation_enabled")
         if cfg.tau != ctx.tau:
             raise ConfigError(f"config tau={cfg.tau} differs from the context's tau={ctx.tau}")
+        if self.use_group and cfg.tau is not None and (ctx.staleness_bound is None or ctx.staleness_bound > cfg.tau):
+            # every endpoint uses staleness_bound=opt.tau (optim.py:386); a
+            # tighter bound is allowed (fault-injection tests), a looser one
+            # would average over-stale replicas silently
+            raise ConfigError(f"context staleness_bound={ctx.staleness_bound} is looser than tau={cfg.tau}")
         self.ctx = ctx
         self.cfg = cfg
         self.T = cfg.T if T is None else T
@@ -158,7 +159,14 @@ class GroupAveragingOptimizer:
 
     def step(self, t: int, grads: Mapping[int, torch.Tensor], *, forced_stamps: Optional[list[int]] = None,
              stream=None) -> None:
-        """Iteration t for every rank in ``grads`` (all local ranks normally)."""
+        """Iteration t for every rank in ``grads`` (all local ranks normally).
+
+        Raises DivergenceError (optim.py:174-175) if an earlier launch
+        produced a non-finite W'; the check reads the host-mapped error word,
+        so it costs no synchronisation and lags the device by the launches in
+        flight (``ctx.check()`` after a synchronise is exact).
+        """
+        self.ctx.check_async()
         versions = {r: t for r in grads}
         forced = {t: forced_stamps} if forced_stamps is not None else None
         self.ctx.launch(self.jobs(versions, grads), forced=forced, stream=stream)
@@ -166,6 +174,7 @@ class GroupAveragingOptimizer:
     def step_mixed(self, versions: Mapping[int, int], grads: Mapping[int, torch.Tensor],
                    forced: Optional[dict[int, list[int]]] = None, stream=None) -> None:
         """One launch in which ranks may be at different iterations (stragglers)."""
+        self.ctx.check_async()
         self.ctx.launch(self.jobs(versions, grads), forced=forced, stream=stream)
 
     def statuses(self) -> list[JobStatus]:
