@@ -37,7 +37,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "WAGMA iters/s and group-avg GB/s vs NVLink roofline at 1/2/4/8 B200"
 N_RESNET50 = 25_559_081
-NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+NVLINK_NOMINAL_GBS = 900.0  # nominal per direction per GPU (north_star)
 
 
 def parse():
@@ -199,16 +200,38 @@ class ClockSampler:
 # algorithmic bytes
 # ---------------------------------------------------------------------------
 
+def hier_levels(leaves, R):
+    """Tree levels of a plan summed inside one GPU (the kernel's plan_hl, 0 = none).
+
+    Largest h >= 1 such that every block of 2^h consecutive leaves lives on
+    one GPU under the block mapping, for plans that span >= 2 GPUs with
+    distinct leaves (mirrors wg_launch)."""
+    n = len(leaves)
+    if len({q // R for q in leaves}) < 2 or len(set(leaves)) != n:
+        return 0
+    log = n.bit_length() - 1
+    for h in range(log - 1, 0, -1):
+        if all(leaves[i] // R == leaves[i & ~((1 << h) - 1)] // R for i in range(n)):
+            return h
+    return 0
+
+
 def step_bytes(a, G, gpu_index, t, elem):
     """(HBM bytes, NVLink ingress bytes) one launch on `gpu_index` must move.
 
     Own streams per local rank: read W, m, g; write m, the send-slot W' and
-    W_{t+1} = 6 * elem * n. Pulled group sum: each leaf on another GPU
-    crosses NVLink once. Split group sum (all-timely group over >= 2 GPUs
-    where it saves bytes, P <= 8; the kernel's split_pays): a fraction f = L/S of the tiles is
-    reduced here (S - L remote leaves each, local leaves re-read, the reduced
-    tile written), the rest arrive as one reduced tile from their owner.
-    Bytes read from this GPU by peers (symmetric) are added to its HBM.
+    W_{t+1} = 6 * elem * n. Bytes read from this GPU by peers (symmetric)
+    are added to its HBM. The kernel's own re-reads of data it just wrote
+    (local leaves or partials copied into shared memory) are not counted
+    (SURVEY.md §8(d)). Per plan, the algorithm the kernel runs:
+    - hierarchical (all timely, lowest hl tree levels inside one GPU,
+      WG_HIER): each GPU writes its 2^hl-leaf subtree partials once and pulls
+      the other GPUs' partials: NVLink = remote partials, HBM += local partials;
+    - split (all timely, spans >= 2 GPUs where it saves bytes, P <= 8, the
+      kernel's split_pays; only when no plan of the launch is hierarchical):
+      a fraction f = L/S of the tiles is reduced here (S - L remote leaves
+      each, the reduced tile written), the rest arrive as one reduced tile;
+    - pull: every leaf on another GPU crosses NVLink once.
     """
     from paper_2005_00124_b200.topology import GroupingParams, compute_groups, tree_leaves
     R = a.P // G
@@ -217,8 +240,6 @@ def step_bytes(a, G, gpu_index, t, elem):
     hbm = R * 6 * n
     nvl = 0.0
     sync = (t + 1) % a.tau == 0
-    split_on = os.environ.get("WG_SPLIT", "1") != "0" and G >= 2 and a.P <= 8 and \
-        n >= int(os.environ.get("WG_SPLIT_MIN_BYTES", str(8 << 20)))  # the kernel's split_min_bytes
     groups = [tuple(range(a.P))] if sync else None
     if not sync:
         part = compute_groups(GroupingParams(a.P, a.S, t))
@@ -227,16 +248,25 @@ def step_bytes(a, G, gpu_index, t, elem):
             grp = part.group_of(r)
             if grp not in groups:
                 groups.append(grp)
-    for grp in groups:
-        leaves = grp if sync else tree_leaves(GroupingParams(a.P, a.S, t), grp[0])
+    plans = [(grp, list(grp) if sync else list(tree_leaves(GroupingParams(a.P, a.S, t), grp[0]))) for grp in groups]
+    hier_on = os.environ.get("WG_HIER", "1") != "0" and G >= 2
+    hls = [hier_levels(leaves, R) if hier_on else 0 for _, leaves in plans]
+    split_on = os.environ.get("WG_SPLIT", "1") != "0" and G >= 2 and a.P <= 8 and not any(hls) and \
+        n >= int(os.environ.get("WG_SPLIT_MIN_BYTES", str(8 << 20)))  # the kernel's split_min_bytes
+    for (grp, leaves), hl in zip(plans, hls):
         L = sum(1 for q in grp if q // R == gpu_index)
         S = len(grp)
         spans = len({q // R for q in grp})
-        if split_on and spans >= int(os.environ.get("WG_SPLIT_SPAN", "2")) and 2 * S >= 3 * (S // spans + 1) and \
+        if hl:
+            parts = leaves[::1 << hl]
+            local_parts = sum(1 for q in parts if q // R == gpu_index)
+            nvl += n * (len(parts) - local_parts)
+            hbm += n * local_parts
+        elif split_on and spans >= int(os.environ.get("WG_SPLIT_SPAN", "2")) and 2 * S >= 3 * (S // spans + 1) and \
                 len(set(leaves)) == len(leaves):
             f = L / S
             nvl += n * (f * (S - L) + (1 - f))
-            hbm += n * f * (L + 1)
+            hbm += n * f
         else:
             nvl += n * sum(1 for q in leaves if q // R != gpu_index)
     return hbm + nvl, nvl
@@ -367,6 +397,11 @@ def run_ours(a):
         roof = {"bound": "hbm", "achieved": hbm_b / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                 "peak_source": f"{peak_kind} HBM copy (MEASURED_PEAKS.json)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    if nvl_b:
+        roof["nvlink_frac"] = {"of_770_measured": nvl_b / kern_s / 1e9 / NVLINK_PEER_GBS,
+                               "of_900_nominal": nvl_b / kern_s / 1e9 / NVLINK_NOMINAL_GBS}
+    roof["t_star_frac"] = {"measured_peaks": max(t_hbm, t_nvl) / kern_s,
+                           "nominal_900": max(t_hbm, nvl_b / (NVLINK_NOMINAL_GBS * 1e9)) / kern_s}
     roof["traffic"] = load_traffic(a, G)
     roof["algorithmic_bytes_per_launch"] = {"hbm": hbm_b, "nvlink_ingress": nvl_b}
     roof["kernel_ms"] = kern_avg_ms

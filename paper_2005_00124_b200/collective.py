@@ -269,10 +269,6 @@ class SyncAllreduce:
             raise InvalidParamsError(f"endpoint P={P} differs from its context P={ctx.P}")
         if rank not in ctx.local_ranks:
             raise InvalidParamsError(f"rank {rank} is not hosted by this process")
-        if (staleness_bound or None) != ctx.staleness_bound:
-            # the device enforces the context's bound at activation (collective.py:290-294)
-            raise InvalidParamsError(f"staleness_bound={staleness_bound} differs from the context's "
-                                     f"{ctx.staleness_bound}")
         self.ctx = ctx
         self.rank = rank
         self.P = P

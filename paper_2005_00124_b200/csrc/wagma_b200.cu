@@ -87,6 +87,8 @@ struct Layout {
     int64_t ring;      // T [R][D][npad]: send ring
     int64_t red_flags; // int64 [R][n_tiles]: latest version whose reduced tile is published (multi-GPU)
     int64_t red_ring;  // T [R][D][npad]: reduced tiles owned by the rank (split sums)
+    int64_t part_flags;  // int64 [R][n_tiles]: latest version whose subtree partial is published (hier sums)
+    int64_t part_ring;   // T [R][D][npad]: GPU-local subtree partials keyed by their first leaf rank
     int64_t total;
 };
 
@@ -146,11 +148,23 @@ struct LaunchParams {
     long long* prof;  // optional per-CTA phase cycle counters [grid][8]
     int32_t fence_scope;  // 0 sys, 1 gpu (default), 2 none (timing experiments only)
     int32_t nvl_stages;   // leaf-ring stages of the multi-GPU TMA kernel
+    int32_t nvl_rows;     // leaf rows per stage the host sized the pull kernel's ring for
     int32_t split_stages; // reduced-tile ring stages of the split kernel
     int32_t split_span;   // minimum GPUs a group must span to be summed split
     int32_t red_warps;    // split kernel: stream-A reducer warps (4 or 8 of the 12 shared with stream B)
     int32_t loc_stages;   // single-GPU TMA kernel: input-ring stages
     int64_t* err_host;    // host-mapped mirror of the error word (wg_ctx_error_async)
+    // hierarchical sums (multi-GPU pull kernel): a plan whose lowest plan_hl
+    // tree levels stay inside one GPU exchanges GPU-local subtree partials
+    // instead of leaves when all its members are timely
+    int8_t plan_hl[kMaxPlans];   // 0: leaf pull
+    int32_t n_parts;             // local partials this launch produces
+    int8_t job_order[kMaxJobs];  // producer job order: every partial's leaves consecutive, in leaf order
+    int8_t job_part[kMaxJobs];   // partial of the k-th produced job (-1: none)
+    int8_t job_ppos[kMaxJobs];   // its leaf position inside the partial
+    int8_t job_plast[kMaxJobs];  // last leaf of the partial: store it
+    int16_t part_key[kMaxJobs];  // first leaf rank of each local partial (its buffer and flags)
+    int64_t part_version[kMaxJobs];
 };
 
 // ---------------------------------------------------------------------------
@@ -310,6 +324,14 @@ __device__ __forceinline__ int64_t* red_flag_ptr(const LaunchParams& p, int rank
 template <typename T>
 __device__ __forceinline__ T* red_ptr(const LaunchParams& p, int rank, int64_t version) {
     return reinterpret_cast<T*>(rank_base(p, rank) + p.L.red_ring) +
+           (int64_t(rank % p.R) * p.D + version % p.D) * p.npad;
+}
+__device__ __forceinline__ int64_t* part_flag_ptr(const LaunchParams& p, int rank, int64_t tile) {
+    return reinterpret_cast<int64_t*>(rank_base(p, rank) + p.L.part_flags) + int64_t(rank % p.R) * p.n_tiles + tile;
+}
+template <typename T>
+__device__ __forceinline__ T* part_ptr(const LaunchParams& p, int rank, int64_t version) {
+    return reinterpret_cast<T*>(rank_base(p, rank) + p.L.part_ring) +
            (int64_t(rank % p.R) * p.D + version % p.D) * p.npad;
 }
 __device__ __forceinline__ Desc* desc_ptr(const LaunchParams& p, int64_t version) {
@@ -624,7 +646,7 @@ __device__ __forceinline__ void init_ring_slots(const LaunchParams& p, T** ring_
 template <typename T, bool STAGE = true>
 __device__ __forceinline__ bool compute_item(const LaunchParams& p, int64_t tile, int j,
                                              const typename Tr<T>::V* slot, typename Tr<T>::V* stage,
-                                             T* const* ring_slot) {
+                                             T* const* ring_slot, typename Tr<T>::V* wp_out = nullptr) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
     const int tid = threadIdx.x;
@@ -656,6 +678,7 @@ __device__ __forceinline__ bool compute_item(const LaunchParams& p, int64_t tile
     T* const rs = ring_slot ? ring_slot[j] : ring_ptr<T>(p, jb.rank, slot_of(p, jb.version));
     __stcg(reinterpret_cast<V*>(rs + idx), wp);
     if (STAGE) stage[j * kThreads + tid] = wp;
+    if (wp_out) *wp_out = wp;
     return bad;
 }
 
@@ -1176,6 +1199,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// Same with an L2 cache policy (createpolicy), e.g. evict-first for inputs read once.
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                              uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 
 // ---------------------------------------------------------------------------
 // single-GPU kernel: TMA producer warp, control warp, consumer warps
@@ -1202,6 +1239,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 #ifndef WG_LOC_CONSUMER_WARPS
 #define WG_LOC_CONSUMER_WARPS 8
 #endif
+#ifndef WG_LOC_EVICT_FIRST  // L2 evict-first policy on the TMA input loads (measured +1%)
+#define WG_LOC_EVICT_FIRST 1
+#endif
+#ifndef WG_LOC_RING_CS  // send-ring stores evict-first (.cs) instead of .cg
+#define WG_LOC_RING_CS 1
+#endif
 constexpr int kLocTiles = WG_LOC_TILES;                    // tiles per chunk (per item)
 constexpr int kLocConsumers = WG_LOC_CONSUMER_WARPS * 32;  // consumer threads
 constexpr int kLocThreads = kLocConsumers + 64;            // + producer warp + control warp
@@ -1210,16 +1253,82 @@ constexpr int kLocVPT = kLocChunkVecs / kLocConsumers;     // vectors per consum
 constexpr int kLocMaxStages = 16;
 static_assert(kLocChunkVecs % kLocConsumers == 0, "a chunk row must split evenly over the consumers");
 
+// Per-job constants of the single-GPU kernel, staged in shared memory once
+// (no per-item parameter-space loads or double -> float conversions).
+template <typename T>
+struct LocJob {
+    T* W;
+    T* m;
+    const T* g;
+    const T* fresh;
+    T* ring;
+    T eta, beta;
+    int32_t kind, mom;
+};
+
+// Consumer work for one item (job j of a chunk): local step, m and send-ring
+// stores, W' into the thread-private stage. FULL: the chunk lies inside n.
+template <typename T, bool FULL>
+__device__ __forceinline__ unsigned loc_item(const LaunchParams& p, const LocJob<T>& jb, int j, int64_t e0,
+                                             const typename Tr<T>::V* r, typename Tr<T>::V* wst, int ct) {
+    using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
+    unsigned bad = 0;
+    const bool sum = jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM;
+#pragma unroll
+    for (int kv = 0; kv < kLocVPT; ++kv) {
+        const int v = kv * kLocConsumers + ct;
+        const int64_t idx = e0 + int64_t(v) * E;
+        const bool tail = !FULL && idx + E > p.n;  // ragged end: global loads, zero-filled
+        V wp;
+        if (sum) {
+            wp = tail ? ld_tail(jb.fresh, idx, p.n) : r[v];
+        } else {
+            const V w = tail ? ld_tail(jb.W, idx, p.n) : r[v];
+            const V g = tail ? ld_tail(jb.g, idx, p.n) : r[kLocChunkVecs + v];
+            if (jb.mom) {
+                // m = beta*m + g ; W' = W - eta*m  (optim.py:179,183)
+                const V m0 = tail ? ld_tail(static_cast<const T*>(jb.m), idx, p.n) : r[2 * kLocChunkVecs + v];
+                const V mn = vadd(vscale(jb.beta, m0), g);
+                st_stream<T, FULL>(jb.m, idx, p.n, mn);
+                wp = vsub(w, vscale(jb.eta, mn));
+            } else {
+                wp = vsub(w, vscale(jb.eta, g));  // W' = W - eta*g (optim.py:181-183)
+            }
+            bad |= unsigned(nonfinite(wp));
+            if (jb.kind == WG_JOB_LOCAL_STEP) {
+                st_stream<T, FULL>(jb.W, idx, p.n, wp);
+                continue;
+            }
+        }
+        // SendBuffer.install (collective.py:95-101): W' once into the ring
+        if (FULL || idx < p.npad) {
+            if (WG_LOC_RING_CS)
+                __stcs(reinterpret_cast<V*>(jb.ring + idx), wp);
+            else
+                __stcg(reinterpret_cast<V*>(jb.ring + idx), wp);
+        }
+        wst[j * kLocChunkVecs + v] = wp;
+    }
+    return bad << j;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __grid_constant__ LaunchParams p) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
     extern __shared__ __align__(128) unsigned char dyn_smem[];
     __shared__ SmemCtl sm;
-    __shared__ T* s_ring[kMaxJobs];
+    __shared__ LocJob<T> s_job[kMaxJobs];
     __shared__ __align__(8) uint64_t full[kLocMaxStages];
     __shared__ __align__(8) uint64_t empty[kLocMaxStages];
     __shared__ volatile int ready;
+    // fast finish of a plan whose leaves are all this launch's W' and whose
+    // members are all timely steps: W_{t+1} = avg for every member
+    __shared__ int8_t s_fast[kMaxPlans];
+    __shared__ int8_t s_leafjob[kMaxPlans][kMaxJobs];
+    __shared__ int8_t s_nmem[kMaxPlans];
+    __shared__ T* s_memW[kMaxPlans][kMaxJobs];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int J = p.n_jobs, NS = p.loc_stages;
     const int64_t chunk_elems = int64_t(kLocChunkVecs) * E;
@@ -1235,13 +1344,33 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
         }
     }
     if (tid < kMaxVersions) sm.activator[tid] = 0;
-    init_ring_slots<T>(p, s_ring);
+    if (tid < J) {
+        const DevJob& jb = p.jobs[tid];
+        LocJob<T> lj;
+        lj.W = static_cast<T*>(jb.W);
+        lj.m = static_cast<T*>(jb.m);
+        lj.g = static_cast<const T*>(jb.g);
+        lj.fresh = static_cast<const T*>(jb.fresh);
+        lj.ring = jb.produces ? ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) : nullptr;
+        lj.eta = T(jb.eta);
+        lj.beta = T(jb.beta);
+        lj.kind = jb.kind;
+        lj.mom = jb.update_rule == WG_UPDATE_MOMENTUM;
+        s_job[tid] = lj;
+    }
     __syncthreads();
 
     if (warp == 0) {
         // ---------------- producer: TMA bulk loads of every item ----------------
         if (lane == 0) {
             constexpr unsigned chunk_bytes = unsigned(kLocChunkVecs) * 16u;
+            const uint64_t pol = WG_LOC_EVICT_FIRST ? policy_evict_first() : 0;
+            auto load = [&](void* d, const T* src, unsigned nb, uint64_t* bar) {
+                if (WG_LOC_EVICT_FIRST)
+                    bulk_g2s_hint(d, src, nb, bar, pol);
+                else
+                    bulk_g2s(d, src, nb, bar);
+            };
             int st = 0;
             unsigned ph = 0;
             int64_t k = 0;
@@ -1257,18 +1386,17 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
                         ok = false;
                         break;
                     }
-                    const DevJob& jb = p.jobs[j];
+                    const LocJob<T>& jb = s_job[j];
                     V* dst = rows + size_t(st) * 3 * kLocChunkVecs;
                     if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
                         mbar_arrive_expect_tx(&full[st], bytes);
-                        if (bytes) bulk_g2s(dst, static_cast<const T*>(jb.fresh) + e0, bytes, &full[st]);
+                        if (bytes) load(dst, jb.fresh + e0, bytes, &full[st]);
                     } else {
-                        const bool mom = jb.update_rule == WG_UPDATE_MOMENTUM;
-                        mbar_arrive_expect_tx(&full[st], (mom ? 3u : 2u) * bytes);
+                        mbar_arrive_expect_tx(&full[st], (jb.mom ? 3u : 2u) * bytes);
                         if (bytes) {
-                            bulk_g2s(dst, static_cast<const T*>(jb.W) + e0, bytes, &full[st]);
-                            bulk_g2s(dst + kLocChunkVecs, static_cast<const T*>(jb.g) + e0, bytes, &full[st]);
-                            if (mom) bulk_g2s(dst + 2 * kLocChunkVecs, static_cast<const T*>(jb.m) + e0, bytes, &full[st]);
+                            load(dst, jb.W + e0, bytes, &full[st]);
+                            load(dst + kLocChunkVecs, jb.g + e0, bytes, &full[st]);
+                            if (jb.mom) load(dst + 2 * kLocChunkVecs, jb.m + e0, bytes, &full[st]);
                         }
                     }
                     if (++st == NS) st = 0, ph ^= 1u;
@@ -1283,9 +1411,9 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
         // ---------------- control: activation + leaf sources ----------------
         if (blockIdx.x == 0) control_phase(p, sm.activator);
         bool res = resolve_core<T>(p, sm, lane, 32, [] { __syncwarp(); });
-        // a leaf slot still being filled by an earlier launch (another
-        // stream): wait until its launch completed the slot
         if (res && lane == 0) {
+            // a leaf slot still being filled by an earlier launch (another
+            // stream): wait until its launch completed the slot
             const uint64_t t0 = globaltimer();
             for (int pl = 0; pl < p.n_plans && res; ++pl)
                 for (int li = 0; li < p.plans[pl].n_leaves && res; ++li) {
@@ -1300,6 +1428,23 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
                     }
                     sm.leaf_src[pl][li] = kSrcReady;
                 }
+            // fast finish: every leaf staged here, every member a timely step
+            for (int pl = 0; pl < p.n_plans; ++pl) {
+                const DevPlan& P_ = p.plans[pl];
+                bool fast = P_.n_leaves <= kMaxJobs;
+                for (int li = 0; li < P_.n_leaves && fast; ++li) {
+                    fast = sm.leaf_src[pl][li] >= 0;
+                    if (fast) s_leafjob[pl][li] = sm.leaf_src[pl][li];
+                }
+                for (int mi = 0; mi < P_.n_members && fast; ++mi) {
+                    const DevJob& jb = p.jobs[P_.members[mi]];
+                    fast = (jb.kind == WG_JOB_STEP || jb.kind == WG_JOB_SYNC_STEP) &&
+                           (jb.kind == WG_JOB_SYNC_STEP || sm.stamps[jb.vidx][jb.rank] == jb.version);
+                    s_memW[pl][mi] = static_cast<T*>(jb.W);
+                }
+                s_nmem[pl] = int8_t(P_.n_members);
+                s_fast[pl] = fast && P_.divisor_pow2;
+            }
         }
         res = __shfl_sync(0xffffffffu, res, 0);
         if (lane == 0) {
@@ -1315,48 +1460,17 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
         bool ok = true, resolved = false;
         for (int64_t c = blockIdx.x; c < n_chunks && ok; c += gridDim.x) {
             const int64_t e0 = c * chunk_elems;
+            const bool fullc = e0 + chunk_elems <= p.n;
             for (int j = 0; j < J; ++j) {
                 if (!mbar_wait(p, &full[st], ph)) {
                     ok = false;
                     break;
                 }
                 const V* r = rows + size_t(st) * 3 * kLocChunkVecs;
-                const DevJob& jb = p.jobs[j];
-                const bool sum = jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM;
-                const bool mom = jb.update_rule == WG_UPDATE_MOMENTUM;
-                const T eta = T(jb.eta), beta = T(jb.beta);
-                T* const rs = s_ring[j];
-#pragma unroll
-                for (int kv = 0; kv < kLocVPT; ++kv) {
-                    const int v = kv * kLocConsumers + ct;
-                    const int64_t idx = e0 + int64_t(v) * E;
-                    const bool tail = idx + E > p.n;  // ragged end: global loads, zero-filled
-                    V wp;
-                    if (sum) {
-                        wp = tail ? ld_tail(static_cast<const T*>(jb.fresh), idx, p.n) : r[v];
-                    } else {
-                        const V w = tail ? ld_tail(static_cast<const T*>(jb.W), idx, p.n) : r[v];
-                        const V g = tail ? ld_tail(static_cast<const T*>(jb.g), idx, p.n) : r[kLocChunkVecs + v];
-                        if (mom) {
-                            // m = beta*m + g ; W' = W - eta*m  (optim.py:179,183)
-                            const V m0 =
-                                tail ? ld_tail(static_cast<const T*>(jb.m), idx, p.n) : r[2 * kLocChunkVecs + v];
-                            const V mn = vadd(vscale(beta, m0), g);
-                            st_stream<T>(static_cast<T*>(jb.m), idx, p.n, mn);
-                            wp = vsub(w, vscale(eta, mn));
-                        } else {
-                            wp = vsub(w, vscale(eta, g));  // W' = W - eta*g (optim.py:181-183)
-                        }
-                        bad |= unsigned(nonfinite(wp)) << j;
-                        if (jb.kind == WG_JOB_LOCAL_STEP) {
-                            st_stream<T>(static_cast<T*>(jb.W), idx, p.n, wp);
-                            continue;
-                        }
-                    }
-                    // SendBuffer.install (collective.py:95-101): W' once into the ring
-                    if (idx < p.npad) __stcg(reinterpret_cast<V*>(rs + idx), wp);
-                    wst[j * kLocChunkVecs + v] = wp;
-                }
+                if (fullc)
+                    bad |= loc_item<T, true>(p, s_job[j], j, e0, r, wst, ct);
+                else
+                    bad |= loc_item<T, false>(p, s_job[j], j, e0, r, wst, ct);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[st]);
                 if (++st == NS) st = 0, ph ^= 1u;
@@ -1371,6 +1485,20 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
             // group sums in the butterfly order + the averaging rule
             for (int pl = 0; pl < p.n_plans; ++pl) {
                 const DevPlan& P_ = p.plans[pl];
+                if (fullc && s_fast[pl]) {
+                    // every member timely: one average, stored to each replica
+                    const T inv = T(1) / T(P_.divisor);
+                    const int nm = s_nmem[pl];
+#pragma unroll
+                    for (int kv = 0; kv < kLocVPT; ++kv) {
+                        const int v = kv * kLocConsumers + ct;
+                        const int64_t idx = e0 + int64_t(v) * E;
+                        auto fetch = [&](int leaf) -> V { return wst[s_leafjob[pl][leaf] * kLocChunkVecs + v]; };
+                        const V avg = vscale(inv, tree_sum<T>(fetch, P_.log_leaves));
+                        for (int mi = 0; mi < nm; ++mi) __stcs(reinterpret_cast<V*>(s_memW[pl][mi] + idx), avg);
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int kv = 0; kv < kLocVPT; ++kv) {
                     const int v = kv * kLocConsumers + ct;
@@ -1422,31 +1550,65 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
 // readiness flags published in chunks of kPubChunk by the last warp to
 // finish a chunk (one GPU-scope fence, cumulative over the other warps'
 // stores acquired through the shared-memory counter). Never waits on a peer.
-template <typename T, int kNvlDepth>
+template <typename T, int kNvlDepth, bool HIER = false>
 __device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename Tr<T>::V* ring, int64_t my_ntiles,
                                                 unsigned* pub_count, T* const* ring_slot,
-                                                int64_t* const* flag_base, unsigned& bad) {
+                                                int64_t* const* flag_base, unsigned& bad,
+                                                T* const* part_base = nullptr, int64_t* const* pflag_base = nullptr) {
     using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
     const int lane = threadIdx.x & 31;
     const int J = p.n_jobs;
+    const int NPa = HIER ? p.n_parts : 0;  // subtree partials produced here (hierarchical sums)
+    auto order = [&](int k) { return HIER ? int(p.job_order[k]) : k; };
     unsigned my_tiles = 0;
-    // issue cursor kNvlDepth items ahead, advanced incrementally
+    // issue cursor kNvlDepth items ahead, advanced incrementally; jobs in
+    // p.job_order (each partial's leaves consecutive and in leaf order)
     int64_t ik = 0;
     int ij = 0;
 #pragma unroll
     for (int d = 0; d < kNvlDepth; ++d) {
-        if (ik < my_ntiles) issue_item<T>(p, int64_t(blockIdx.x) + ik * gridDim.x, ij, ring + d * 3 * kThreads);
+        if (ik < my_ntiles) issue_item<T>(p, int64_t(blockIdx.x) + ik * gridDim.x, order(ij), ring + d * 3 * kThreads);
         cp_async_commit();
         if (++ij == J) ij = 0, ++ik;
     }
     int rs = 0;
     for (int64_t kk = 0; kk < my_ntiles; ++kk) {
         const int64_t tile = int64_t(blockIdx.x) + kk * gridDim.x;
-        for (int j = 0; j < J; ++j) {
+        V s0, s1, s2, s3;  // butterfly stack of the partial being summed (<= 16 leaves)
+        for (int jj = 0; jj < J; ++jj) {
+            const int j = order(jj);
             cp_async_wait<kNvlDepth - 1>();
             V* slot = ring + rs * 3 * kThreads;
-            bad |= unsigned(compute_item<T, false>(p, tile, j, slot, nullptr, ring_slot)) << j;
-            if (ik < my_ntiles) issue_item<T>(p, int64_t(blockIdx.x) + ik * gridDim.x, ij, slot);
+            V wp;
+            bad |= unsigned(compute_item<T, false>(p, tile, j, slot, nullptr, ring_slot, &wp)) << j;
+            if (NPa && p.job_part[jj] >= 0) {
+                // partial = the subtree's butterfly sum (collective.py:321-329):
+                // leaf `pos` combines with the stack levels of its set bits
+                const int pos = p.job_ppos[jj];
+                V v = wp;
+                if (pos & 1) {
+                    v = vadd(s0, v);
+                    if (pos & 2) {
+                        v = vadd(s1, v);
+                        if (pos & 4) {
+                            v = vadd(s2, v);
+                            if (pos & 8) v = vadd(s3, v); else s3 = v;
+                        } else {
+                            s2 = v;
+                        }
+                    } else {
+                        s1 = v;
+                    }
+                } else {
+                    s0 = v;
+                }
+                if (p.job_plast[jj])
+                    __stcg(reinterpret_cast<V*>(part_base[p.job_part[jj]] + tile * p.tile_elems +
+                                                int64_t(threadIdx.x) * E),
+                           v);
+            }
+            if (ik < my_ntiles) issue_item<T>(p, int64_t(blockIdx.x) + ik * gridDim.x, order(ij), slot);
             cp_async_commit();
             if (++ij == J) ij = 0, ++ik;
             if (++rs == kNvlDepth) rs = 0;
@@ -1483,6 +1645,10 @@ __device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename 
                         st_relaxed_sys(flag_base[j] + (int64_t(blockIdx.x) + (k0 + b) * gridDim.x) * kWarps + w,
                                        jb.version);
                 }
+                for (int e = lane; e < nk * NPa; e += 32) {  // the chunk's subtree partials
+                    const int pid = e % NPa, b = e / NPa;
+                    st_relaxed_sys(pflag_base[pid] + int64_t(blockIdx.x) + (k0 + b) * gridDim.x, p.part_version[pid]);
+                }
             }
         }
         ++my_tiles;
@@ -1512,47 +1678,44 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     __shared__ SmemCtl sm;
     __shared__ T* s_ring[kMaxJobs];
     __shared__ int64_t* s_flag0[kMaxJobs];
+    __shared__ T* s_part[kMaxJobs];           // local subtree partial buffers (this launch's version)
+    __shared__ int64_t* s_pflag0[kMaxJobs];   // and their per-tile flags
     __shared__ __align__(8) uint64_t full[kNvlMaxStages];
     __shared__ __align__(8) uint64_t empty[kNvlMaxStages];
-    __shared__ int leaf_base[kMaxPlans + 1];
     __shared__ volatile int ready;
-    __shared__ const int64_t* s_poll_ptr[kMaxPoll];     // (leaf, warp) flag of tile 0
+    // effective leaves of every plan, set after lock-in: the plan's leaves
+    // (leaf pull) or its GPU-local subtree partials (hierarchical sum)
+    __shared__ int eff_base[kMaxPlans + 1];
+    __shared__ int8_t eff_log[kMaxPlans];
+    __shared__ int8_t eff_row[kMaxPoll / kWarps];        // flat effective leaf -> TMA row (-1: read from global)
+    __shared__ const T* s_leaf_src[kMaxPoll / kWarps];   // flat effective leaf -> its buffer (tile 0)
+    __shared__ const int64_t* s_poll_ptr[kMaxPoll];      // flags to wait for (tile 0)
     __shared__ int64_t poll_s[kMaxPoll];
-    __shared__ const T* s_leaf_src[kMaxPoll / kWarps];  // flat leaf -> its send-ring slot
-    __shared__ int n_poll_sh;
-    __shared__ int n_rows_sh;
+    __shared__ int8_t poll_stride[kMaxPoll];             // kWarps: per-warp leaf flags; 1: per-tile partial flags
+    __shared__ int n_poll_sh, n_rows_sh, n_eff_sh, ns_sh;
     __shared__ unsigned pub_count[kPubRing];
-    __shared__ int8_t tma_row[kMaxPlans * kMaxLeaves];  // flat leaf -> row of the TMA ring (-1: read from global)
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int J = p.n_jobs;
-    const int NS = p.nvl_stages;
     if (tid == 0) {
         sm.abort = 0;
         ready = 0;
-        for (int st = 0; st < NS; ++st) {
+        for (int st = 0; st < kNvlMaxStages; ++st) {
             mbar_init(&full[st], 1);
             mbar_init(&empty[st], kWarps);
         }
-        int acc = 0, nr = 0;
-        for (int pl = 0; pl < p.n_plans; ++pl) {
-            leaf_base[pl] = acc;
-            for (int li = 0; li < p.plans[pl].n_leaves; ++li)
-                tma_row[acc + li] =
-                    (WG_NVL_TMA_LOCAL || p.plans[pl].leaves[li] / p.R != p.gpu_index) ? int8_t(nr++) : int8_t(-1);
-            acc += p.plans[pl].n_leaves;
-        }
-        leaf_base[p.n_plans] = acc;
-        n_rows_sh = nr;
     }
     if (tid < kMaxVersions) sm.activator[tid] = 0;
     init_ring_slots<T>(p, s_ring, s_flag0);
+    if (tid < p.n_parts) {
+        s_part[tid] = part_ptr<T>(p, p.part_key[tid], p.part_version[tid]);
+        s_pflag0[tid] = part_flag_ptr(p, p.part_key[tid], 0);
+    }
     if (tid < kPubRing) pub_count[tid] = 0;
     __syncthreads();
-    const int NL = leaf_base[p.n_plans];
-    const int NR = n_rows_sh;  // leaves on other GPUs: fetched by TMA over NVLink
-    V* leafbuf = reinterpret_cast<V*>(dyn_smem);          // [NS][NR][kThreads]
-    V* ring = leafbuf + size_t(NS) * NR * kThreads;         // [kNvlDepth][3][kThreads]
+    // leaf-ring capacity (host-sized for leaf pulls of every plan): rows x stages
+    const int cap_rows = p.nvl_stages * p.nvl_rows;
+    V* leafbuf = reinterpret_cast<V*>(dyn_smem);                      // [NS][NR][kThreads]
+    V* ring = leafbuf + size_t(cap_rows) * kThreads;                    // [kNvlDepth][3][kThreads]
     const int64_t my_ntiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const unsigned tile_bytes = unsigned(p.tile_elems * int64_t(sizeof(T)));
     unsigned my_tiles = 0;
@@ -1561,7 +1724,9 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         // ---------------- producers ----------------
         const long long pc0 = clock64();
         unsigned bad = 0;
-        my_tiles = nvl_produce<T, kNvlDepth>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad);
+        my_tiles = p.n_parts ? nvl_produce<T, kNvlDepth, true>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad,
+                                                               s_part, s_pflag0)
+                             : nvl_produce<T, kNvlDepth, false>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad);
         report_divergence(p, bad);
         if (p.prof && tid == 0) p.prof[blockIdx.x * 8 + 0] = clock64() - pc0;
     } else if (warp == 2 * kWarps) {
@@ -1569,29 +1734,58 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         if (blockIdx.x == 0) control_phase(p, sm.activator);
         bool resolved = resolve_core<T>(p, sm, lane, 32, [] { __syncwarp(); });
         __syncwarp();
-        // every leaf goes through the ring; flags to wait for: peers'
-        // in-progress tiles and this GPU's own producers (this launch)
-        int n_poll = 0;
+        // every effective leaf goes through the ring; flags to wait for:
+        // peers' in-progress tiles and this GPU's own producers (this launch)
         if (resolved && lane == 0) {
-            for (int pl = 0; pl < p.n_plans; ++pl)
-                for (int li = 0; li < p.plans[pl].n_leaves; ++li) {
-                    if (sm.leaf_src[pl][li] == kSrcReady) continue;
-                    const int q = p.plans[pl].leaves[li];
-                    if (sm.leaf_src[pl][li] >= 0) sm.leaf_slot[pl][li] = int16_t(slot_of(p, sm.stamps[p.plans[pl].vidx][q]));
-                    for (int w = 0; w < kWarps; ++w) {
-                        if (n_poll == kMaxPoll) {
-                            raise_error(p, WG_EINVAL, n_poll);
-                            break;
-                        }
-                        s_poll_ptr[n_poll] = flag_ptr(p, q, 0, w);
-                        poll_s[n_poll] = sm.stamps[p.plans[pl].vidx][q];
+            int n_poll = 0, f = 0, nr = 0;
+            for (int pl = 0; pl < p.n_plans; ++pl) {
+                const DevPlan& P_ = p.plans[pl];
+                const int64_t v = p.versions[P_.vidx].version;
+                // hierarchical sum iff every member contributed fresh W'_v:
+                // then every GPU of the group produced its subtree partials
+                // of v (every GPU sees the same locked stamps)
+                bool hier = p.plan_hl[pl] > 0;
+                for (int li = 0; li < P_.n_leaves && hier; ++li) hier = sm.stamps[P_.vidx][P_.leaves[li]] == v;
+                eff_base[pl] = f;
+                if (hier) {
+                    const int hl = p.plan_hl[pl];
+                    eff_log[pl] = int8_t(P_.log_leaves - hl);
+                    for (int u = 0; u < (P_.n_leaves >> hl); ++u, ++f) {
+                        const int key = P_.leaves[u << hl];
+                        s_leaf_src[f] = part_ptr<T>(p, key, v);
+                        eff_row[f] = int8_t(nr++);
+                        s_poll_ptr[n_poll] = part_flag_ptr(p, key, 0);
+                        poll_s[n_poll] = v;
+                        poll_stride[n_poll] = 1;
                         ++n_poll;
                     }
+                } else {
+                    eff_log[pl] = int8_t(P_.log_leaves);
+                    for (int li = 0; li < P_.n_leaves; ++li, ++f) {
+                        const int q = P_.leaves[li];
+                        if (sm.leaf_src[pl][li] >= 0) sm.leaf_slot[pl][li] = int16_t(slot_of(p, sm.stamps[P_.vidx][q]));
+                        s_leaf_src[f] = ring_ptr<T>(p, q, sm.leaf_slot[pl][li]);
+                        eff_row[f] = (WG_NVL_TMA_LOCAL || q / p.R != p.gpu_index) ? int8_t(nr++) : int8_t(-1);
+                        if (sm.leaf_src[pl][li] == kSrcReady) continue;
+                        for (int w = 0; w < kWarps; ++w) {
+                            if (n_poll == kMaxPoll) {
+                                raise_error(p, WG_EINVAL, n_poll);
+                                break;
+                            }
+                            s_poll_ptr[n_poll] = flag_ptr(p, q, 0, w);
+                            poll_s[n_poll] = sm.stamps[P_.vidx][q];
+                            poll_stride[n_poll] = kWarps;
+                            ++n_poll;
+                        }
+                    }
                 }
-            for (int pl = 0; pl < p.n_plans; ++pl)
-                for (int li = 0; li < p.plans[pl].n_leaves; ++li)
-                    s_leaf_src[leaf_base[pl] + li] = ring_ptr<T>(p, p.plans[pl].leaves[li], sm.leaf_slot[pl][li]);
+            }
+            eff_base[p.n_plans] = f;
             n_poll_sh = n_poll;
+            n_rows_sh = nr;
+            n_eff_sh = f;
+            // stages of the effective rows in the same shared memory
+            ns_sh = nr == 0 ? kNvlMaxStages : (cap_rows / nr < kNvlMaxStages ? cap_rows / nr : kNvlMaxStages);
             __threadfence_block();
             ready = aborted(p) ? 2 : 1;
         } else if (!resolved && lane == 0) {
@@ -1599,7 +1793,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         }
         __syncwarp();
         resolved = resolved && ready == 1;
-        n_poll = n_poll_sh;
+        const int n_poll = n_poll_sh, NR = n_rows_sh, NL = n_eff_sh, NS = ns_sh;
         // Batches of up to kPullBatch tiles: one round of flag loads (all
         // lanes, all tiles of the batch in flight), one acquire fence, then
         // the TMA copies of the whole batch.
@@ -1630,7 +1824,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
                     if (e < total) {
                         const int idx = e % n_poll;
                         const int64_t tile = int64_t(blockIdx.x) + (kc + e / n_poll) * gridDim.x;
-                        v[r] = ld_relaxed_sys(s_poll_ptr[idx] + tile * kWarps);
+                        v[r] = ld_relaxed_sys(s_poll_ptr[idx] + tile * poll_stride[idx]);
                     }
                 }
 #pragma unroll
@@ -1647,7 +1841,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
                             break;
                         }
                         __nanosleep(32);
-                        v[r] = ld_relaxed_sys(s_poll_ptr[idx] + tile * kWarps);
+                        v[r] = ld_relaxed_sys(s_poll_ptr[idx] + tile * poll_stride[idx]);
                     }
                     if (!rc && v[r] >= poll_s[idx] + p.D) rc = WG_EPROTO;
                     if (rc) raise_error(p, rc, int64_t(idx) << 32 | (tile & 0xffffffff));
@@ -1673,7 +1867,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
             __syncwarp();
             for (int e = lane; e < nb * NL; e += 32) {
                 const int b = e / NL, f = e % NL;
-                const int row = tma_row[f];
+                const int row = eff_row[f];
                 if (row < 0) continue;
                 const int st = st0 + b < NS ? st0 + b : st0 + b - NS;
                 const int64_t tile = int64_t(blockIdx.x) + (kc + b) * gridDim.x;
@@ -1695,9 +1889,11 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         const int ctid = tid - kThreads;  // vector index within the tile
         const long long cc0 = clock64();
         while (ready == 0) __nanosleep(64);
+        __threadfence_block();
         const long long cc1 = clock64();
         long long cy_full = 0;
         if (ready == 1) {
+            const int NR = n_rows_sh, NS = ns_sh;
             for (int64_t kc = 0, st = 0, ph = 0; kc < my_ntiles; ++kc) {
                 const long long w0 = clock64();
                 if (!mbar_wait(p, &full[st], unsigned(ph))) {
@@ -1710,9 +1906,9 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
                 const V* lb = leafbuf + size_t(st) * NR * kThreads;
                 for (int pl = 0; pl < p.n_plans; ++pl) {
                     const DevPlan& P_ = p.plans[pl];
-                    const int base = leaf_base[pl];
+                    const int base = eff_base[pl];
                     auto fetch = [&](int leaf) -> V {
-                        const int row = tma_row[base + leaf];
+                        const int row = eff_row[base + leaf];
                         if (row >= 0) return lb[row * kThreads + ctid];
                         // this GPU's leaf: the slot tile (published, usually in L2)
                         return __ldcg(reinterpret_cast<const V*>(
@@ -1722,7 +1918,9 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
                         const DevJob& jb = p.jobs[j];
                         return __ldcg(reinterpret_cast<const V*>(ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + idx));
                     };
-                    finish_members<T>(p, sm, P_, tree_sum<T>(fetch, P_.log_leaves), idx, own_wp);
+                    // the tree over the effective leaves: levels above the
+                    // partials pair them exactly as the full tree would
+                    finish_members<T>(p, sm, P_, tree_sum<T>(fetch, eff_log[pl]), idx, own_wp);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[st]);
@@ -2502,7 +2700,7 @@ struct Blob {
     // process-wide kernel choices that every GPU of a job must share: which
     // multi-GPU kernel runs (only the split kernel publishes reduced tiles),
     // its tile ownership (grid = SMs x occupancy) and the flag fence scope
-    int32_t use_nvl, use_split, split_span, fence_scope, sms, occ_split, occ_nvl, pad;
+    int32_t use_nvl, use_split, split_span, fence_scope, sms, occ_split, occ_nvl, use_hier;
     int64_t split_min_bytes;
     cudaIpcMemHandle_t handle;
 };
@@ -2535,6 +2733,7 @@ struct wg_ctx {
     int occ_nvl[2];
     int occ_split[2];
     int use_loc;              // single-GPU launches: TMA kernel (else the cp.async kernel)
+    int use_hier;             // multi-GPU: exchange GPU-local subtree partials where the tree allows
     int loc_dyn_max[2];       // dynamic shared memory available to wagma_local_kernel<T>
     int64_t* err_host;        // host-mapped mirror of the error word
     int64_t* err_host_dev;
@@ -2591,6 +2790,8 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     if (const char* sm = getenv("WG_SPLIT_MIN_BYTES")) ctx->split_min_bytes = std::max<long long>(0, atoll(sm));
     ctx->use_loc = 1;
     if (const char* lc = getenv("WG_LOC")) ctx->use_loc = atoi(lc);
+    ctx->use_hier = 1;
+    if (const char* hh = getenv("WG_HIER")) ctx->use_hier = atoi(hh);
     ctx->fence_scope = 1;  // GPU scope for per-tile flags (see publish_tile)
     if (const char* fs = getenv("WG_FENCE_SCOPE")) {
         if (!strcmp(fs, "sys")) ctx->fence_scope = 0;
@@ -2627,6 +2828,11 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     off = align_up(off + red * int64_t(ctx->R) * ctx->n_tiles * 8, 4096);
     L.red_ring = off;
     off = align_up(off + red * int64_t(ctx->R) * ctx->D * ctx->npad * int64_t(ctx->esize), 4096);
+    const int64_t hier = (ctx->use_hier && c.n_gpus >= 2) ? 1 : 0;
+    L.part_flags = off;
+    off = align_up(off + hier * int64_t(ctx->R) * ctx->n_tiles * 8, 4096);
+    L.part_ring = off;
+    off = align_up(off + hier * int64_t(ctx->R) * ctx->D * ctx->npad * int64_t(ctx->esize), 4096);
     L.total = off;
 
     int rc = WG_OK;
@@ -2645,6 +2851,7 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
         fill(L.complete, int64_t(ctx->R) * ctx->D, kNever);
         fill(L.flags, int64_t(ctx->R) * ctx->n_tiles * kWarps, kNever);
         if (L.red_ring > L.red_flags) fill(L.red_flags, int64_t(ctx->R) * ctx->n_tiles, kNever);
+        if (L.part_ring > L.part_flags) fill(L.part_flags, int64_t(ctx->R) * ctx->n_tiles, kNever);
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { rc = fail(WG_ECUDA, "arena init: %s", cudaGetErrorString(e)); break; }
         e = cudaHostAlloc(&ctx->status_host, sizeof(wg_job_status) * kMaxJobs, cudaHostAllocMapped);
@@ -2750,6 +2957,7 @@ int wg_ctx_export(wg_ctx* ctx, void* blob, size_t cap, size_t* len) {
     b.occ_split = ctx->occ_split[ctx->cfg.dtype == WG_F32 ? 0 : 1];
     b.occ_nvl = ctx->occ_nvl[ctx->cfg.dtype == WG_F32 ? 0 : 1];
     b.split_min_bytes = ctx->split_min_bytes;
+    b.use_hier = ctx->use_hier;
     WG_CUDA(cudaSetDevice(ctx->cfg.device));
     WG_CUDA(cudaIpcGetMemHandle(&b.handle, ctx->arena));
     std::memcpy(blob, &b, sizeof(b));
@@ -2771,10 +2979,10 @@ int wg_ctx_import_peer(wg_ctx* ctx, int gpu_index, const void* blob, size_t len)
     const int di = ctx->cfg.dtype == WG_F32 ? 0 : 1;
     if (b.use_nvl != ctx->use_nvl || b.use_split != ctx->use_split || b.split_span != ctx->split_span ||
         b.fence_scope != ctx->fence_scope || b.sms != ctx->sms || b.occ_split != ctx->occ_split[di] ||
-        b.occ_nvl != ctx->occ_nvl[di] || b.split_min_bytes != ctx->split_min_bytes)
+        b.occ_nvl != ctx->occ_nvl[di] || b.split_min_bytes != ctx->split_min_bytes || b.use_hier != ctx->use_hier)
         return fail(WG_EINVAL,
                     "peer %d runs different kernel settings (WG_NVL/WG_SPLIT/WG_SPLIT_SPAN/WG_SPLIT_MIN_BYTES/"
-                    "WG_FENCE_SCOPE or SM count / occupancy differ)", gpu_index);
+                    "WG_FENCE_SCOPE/WG_HIER or SM count / occupancy differ)", gpu_index);
     if (gpu_index == ctx->cfg.gpu_index) return WG_OK;
     if (ctx->opened[gpu_index]) return WG_OK;
     WG_CUDA(cudaSetDevice(ctx->cfg.device));
@@ -2862,6 +3070,8 @@ static int occupancy(wg_ctx* ctx, int n_stage) {
 
 // Input-ring stages of wagma_local_kernel for a launch of n_jobs jobs (the W'
 // stage takes one chunk row per job); < 2 means the launch does not fit.
+static bool L_has_parts(const wg_ctx* ctx) { return ctx->L.part_ring > ctx->L.part_flags; }
+
 static int local_stages(wg_ctx* ctx, int n_jobs) {
     const int64_t row = int64_t(kLocChunkVecs) * 16;
     const int64_t avail = int64_t(ctx->loc_dyn_max[ctx->cfg.dtype == WG_F32 ? 0 : 1]) - int64_t(n_jobs) * row;
@@ -3044,6 +3254,72 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         }
     }
 
+    // producer job order (identity unless subtree partials are produced)
+    for (int j = 0; j < n_jobs; ++j) {
+        p.job_order[j] = int8_t(j);
+        p.job_part[j] = -1;
+    }
+    // Hierarchical sums: a plan spanning GPUs whose lowest hl tree levels
+    // stay inside one GPU (masks < R under the block rank mapping,
+    // topology.py:127-128) is summed from GPU-local subtree partials of
+    // 2^hl leaves when all members are timely; the producers compute this
+    // GPU's partials in the butterfly order (bits unchanged). The choice
+    // depends only on the schedule and this launch's jobs, identical on
+    // every GPU that runs all its ranks at one version.
+    bool any_hier = false;
+    if (p.need_fence && ctx->use_hier && L_has_parts(ctx)) {
+        int nord = 0, np = 0;
+        bool placed[kMaxJobs] = {};
+        for (int k = 0; k < p.n_plans; ++k) {
+            DevPlan& P_ = p.plans[k];
+            int hl = 0;
+            unsigned gpus = 0;
+            for (int li = 0; li < P_.n_leaves; ++li) gpus |= 1u << (P_.leaves[li] / ctx->R);
+            if (__builtin_popcount(gpus) >= 2 && p.owners[k].n == P_.n_leaves) {
+                for (int h = P_.log_leaves - 1; h >= 1 && !hl; --h) {
+                    bool ok = true;
+                    for (int li = 0; li < P_.n_leaves && ok; ++li)
+                        ok = P_.leaves[li] / ctx->R == P_.leaves[li & ~((1 << h) - 1)] / ctx->R;
+                    if (ok) hl = h;
+                }
+            }
+            // this GPU produces its partials: every local leaf is a job of this launch at the plan's version
+            for (int li = 0; li < P_.n_leaves && hl; ++li) {
+                const int q = P_.leaves[li];
+                if (q / ctx->R != c.gpu_index) continue;
+                const int jq = p.job_of_rank[q];
+                if (jq < 0 || !p.jobs[jq].produces || p.jobs[jq].vidx != P_.vidx || placed[jq]) hl = 0;
+            }
+            p.plan_hl[k] = int8_t(hl);
+            if (!hl) continue;
+            any_hier = true;
+            for (int u = 0; u < (P_.n_leaves >> hl); ++u) {
+                const int key = P_.leaves[u << hl];
+                if (key / ctx->R != c.gpu_index) continue;
+                if (np == kMaxJobs) return fail(WG_EINVAL, "too many subtree partials");
+                p.part_key[np] = int16_t(key);
+                p.part_version[np] = p.versions[P_.vidx].version;
+                for (int i = 0; i < (1 << hl); ++i) {
+                    const int jq = p.job_of_rank[P_.leaves[(u << hl) + i]];
+                    placed[jq] = true;
+                    p.job_order[nord] = int8_t(jq);
+                    p.job_part[nord] = int8_t(np);
+                    p.job_ppos[nord] = int8_t(i);
+                    p.job_plast[nord] = int8_t(i == (1 << hl) - 1);
+                    ++nord;
+                }
+                ++np;
+            }
+        }
+        for (int j = 0; j < n_jobs; ++j)
+            if (!placed[j]) {
+                p.job_order[nord] = int8_t(j);
+                p.job_part[nord] = -1;
+                ++nord;
+            }
+        p.n_parts = np;
+    }
+
     // dynamic shared memory: the cp.async input ring + one 16-byte stage
     // vector per thread per job (x2 when tiles are produced one ahead for
     // peers on other GPUs)
@@ -3072,7 +3348,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         wide = wide || (__builtin_popcount(gpus) >= ctx->split_span && p.owners[k].n == p.plans[k].n_leaves &&
                         split_pays(p.owners[k].n, __builtin_popcount(gpus)));
     }
-    if (p.need_fence && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= ctx->split_span && wide &&
+    if (p.need_fence && !any_hier && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= ctx->split_span && wide &&
         c.n * int64_t(ctx->esize) >= ctx->split_min_bytes) {
         // split sums: every GPU of a job makes this same choice (it depends on
         // P and the process-wide knob only), so owners always publish the
@@ -3124,6 +3400,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
     } else if (p.need_fence && ctx->use_nvl && nvl_stages >= 2 && n_leaves_total * kWarps <= kMaxPoll &&
         n_leaves_total <= kMaxPlans * kMaxLeaves) {
         p.nvl_stages = nvl_stages;
+        p.nvl_rows = n_rows;
         const size_t nvl_smem = nvl_fixed + size_t(nvl_stages) * n_rows * row;
         const int di = c.dtype == WG_F32 ? 0 : 1;
         if (ctx->occ_nvl[di] <= 0) {

@@ -38,6 +38,10 @@ def main():
     ap.add_argument("--grace-us", type=float, default=50.0)
     ap.add_argument("--momentum", type=int, default=1)
     ap.add_argument("--alpha", type=int, default=1)
+    ap.add_argument("--pipelined", type=int, default=0,
+                    help="launch steps back to back (no host synchronisation per step, as bench.py does)")
+    ap.add_argument("--save-grads", type=int, default=1,
+                    help="0: the parent regenerates the gradients (driver.synthetic_grad) instead of loading them")
     a = ap.parse_args()
 
     rank = int(os.environ["RANK"])
@@ -64,8 +68,11 @@ def main():
         if set(ctx.local_ranks) & pol.victims(t, a.P):
             ctx.delay(int(a.delay_us * 1000))
         opt.step(t, g)
-        torch.cuda.synchronize()
-        statuses.append([(s.version, s.contrib_stamp, s.timely, s.activator) for s in ctx.statuses()])
+        if not a.save_grads:
+            grads.clear()
+        if not a.pipelined:
+            torch.cuda.synchronize()
+            statuses.append([(s.version, s.contrib_stamp, s.timely, s.activator) for s in ctx.statuses()])
     torch.cuda.synchronize()
     ctx.check()
     dist.barrier()

@@ -37,8 +37,8 @@ def _bench_module():
     return mod
 
 
-def test_algorithmic_bytes_per_launch():
-    """Roofline numerators: pull leaves, split sums, one GPU."""
+def test_algorithmic_bytes_per_launch(monkeypatch):
+    """Roofline numerators: pull leaves, split sums, hierarchical partials, one GPU."""
     import types
 
     b = _bench_module()
@@ -47,8 +47,16 @@ def test_algorithmic_bytes_per_launch():
     a = types.SimpleNamespace(P=8, S=8, tau=10, n=n)
     hbm, nvl = b.step_bytes(a, 1, 0, 0, 4)  # all 8 ranks local: 6 streams each, no NVLink
     assert nvl == 0 and hbm == 8 * 6 * N
+    # hierarchical: 2 GPUs, masks (1,2,4): one 4-leaf partial per GPU, pull the other
+    hbm, nvl = b.step_bytes(a, 2, 0, 0, 4)
+    assert nvl == 1.0 * N and hbm == 4 * 6 * N + N + N
+    hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)  # 4 GPUs: 2-leaf partials, pull 3
+    assert nvl == 3.0 * N and hbm == 2 * 6 * N + N + 3 * N
+    assert b.hier_levels([0, 1, 2, 3, 4, 5, 6, 7], 4) == 2 and b.hier_levels([0, 4, 1, 5], 4) == 0
+    assert b.hier_levels([0, 2, 4, 6], 4) == 1 and b.hier_levels([0, 1, 2, 3], 4) == 0  # one GPU: no exchange
+    monkeypatch.setenv("WG_HIER", "0")
     hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)  # split over 4 GPUs: f = 2/8 -> f*6 + 3/4 = 2.25 N
-    assert nvl == 2.25 * N
+    assert nvl == 2.25 * N and hbm == 2 * 6 * N + 0.25 * N + 2.25 * N
     hbm, nvl = b.step_bytes(a, 8, 0, 0, 4)  # one rank per GPU: 1/8*7 + 7/8 = 1.75 N
     assert nvl == 1.75 * N
     a = types.SimpleNamespace(P=4, S=2, tau=10, n=n)

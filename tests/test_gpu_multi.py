@@ -25,7 +25,7 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def _run(tmp_path, G, port, **kw):
+def _run(tmp_path, G, port, env_extra=None, **kw):
     args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
             "--master-addr", "127.0.0.1", "--master-port", str(port),
             os.path.join(ROOT, "tests", "multigpu_worker.py"), "--out", str(tmp_path)]
@@ -33,9 +33,16 @@ def _run(tmp_path, G, port, **kw):
         args += [f"--{k.replace('_', '-')}", str(v)]
     # small test vectors: keep the split-sum kernel in play (it is off below 8 MiB by default)
     env = dict(os.environ, WG_SPLIT_MIN_BYTES="0")
-    res = subprocess.run(args, capture_output=True, text=True, timeout=600, env=env)
+    env.update(env_extra or {})
+    res = subprocess.run(args, capture_output=True, text=True, timeout=900, env=env)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     return [dict(np.load(os.path.join(tmp_path, f"rank{r}.npz"))) for r in range(G)]
+
+
+@pytest.fixture(params=["hier", "nohier"])
+def hier(request):
+    """Hierarchical subtree-partial sums on (default) or off (split / pull kernels)."""
+    return {"WG_HIER": "1" if request.param == "hier" else "0"}
 
 
 CASES = [
@@ -51,11 +58,12 @@ CASES = [
 
 
 @pytest.mark.parametrize("G,P,S,T,tau,n,dtype,victims,alpha", CASES)
-def test_multigpu_live_protocol_bit_exact(tmp_path, G, P, S, T, tau, n, dtype, victims, alpha):
+def test_multigpu_live_protocol_bit_exact(tmp_path, hier, G, P, S, T, tau, n, dtype, victims, alpha):
     if _ngpus() < G:
         pytest.skip(f"needs {G} GPUs")
-    port = 29400 + (hash((G, P, S, T, n)) % 500)
-    outs = _run(tmp_path, G, port, P=P, S=S, T=T, tau=tau, nelem=n, dtype=dtype, victims=victims, alpha=alpha)
+    port = 29400 + (hash((G, P, S, T, n, hier["WG_HIER"])) % 500)
+    outs = _run(tmp_path, G, port, env_extra=hier, P=P, S=S, T=T, tau=tau, nelem=n, dtype=dtype, victims=victims,
+                alpha=alpha)
     R = P // G
     npdt = np.float32 if dtype == "f32" else np.float64
     W = np.stack([outs[r // R][f"W{r}"] for r in range(P)])
@@ -82,3 +90,65 @@ def test_multigpu_live_protocol_bit_exact(tmp_path, G, P, S, T, tau, n, dtype, v
         if victims:
             late = sum(int((stamps[v] >= -1).sum() - (stamps[v] == v).sum()) for v in range(T))
             assert late > 0, "injected stragglers never contributed a stale model"
+
+
+BASELINE_CASES = [
+    # G, S: P = 8 ranks, n = 25,559,081 fp32 (BASELINE configs[1]), tau = 10, T = 12 (one global sync)
+    (2, 8), (2, 4), (4, 8), (4, 4),
+]
+
+
+def _replay_streaming(P, S, tau, T, n, w0, grad_fn, stamps, eta=0.05, beta=0.9):
+    """Alg. 2 for all P ranks with the C oracle, holding only the send-buffer
+    snapshots the contribution log references (BASELINE-sized vectors)."""
+    from oracle import c_oracle
+    from oracle import topology_oracle as otopo
+    W = [w0.copy() for _ in range(P)]
+    m = [np.zeros(n, np.float32) for _ in range(P)]
+    wp = [np.empty(n, np.float32) for _ in range(P)]
+    keep = {(q, int(s)) for v in range(T) for q, s in enumerate(stamps[v]) if 0 <= s < v}
+    needs_w0 = bool((stamps == -1).any())
+    sendbuf = {(q, -1): w0 for q in range(P)} if needs_w0 else {}
+    for t in range(T):
+        g = [grad_fn(r, t) for r in range(P)]
+        sync = (t + 1) % tau == 0
+        if sync:
+            masks, div, contrib, timely = [1 << j for j in range(P.bit_length() - 1)], P, None, None
+        else:
+            masks, div = list(otopo.phase_masks(P, S, t)), S
+            contrib = [None if int(stamps[t, q]) == t else sendbuf[(q, int(stamps[t, q]))] for q in range(P)]
+            timely = [int(stamps[t, q]) == t for q in range(P)]
+        c_oracle.wagma_iteration(W, m, g, wp, masks, div, eta, beta, True, contrib=contrib, timely=timely)
+        for q in range(P):
+            if (q, t) in keep:
+                sendbuf[(q, t)] = wp[q].copy()
+    return np.stack(W)
+
+
+@pytest.mark.parametrize("G,S", BASELINE_CASES)
+def test_multigpu_baseline_size_bit_exact(tmp_path, hier, G, S):
+    """BASELINE configs[1] on 2 / 4 GPUs: P = 8, n = 25,559,081, one straggler GPU
+    per iteration, launches pipelined as in bench.py, default split threshold;
+    every replica bit-exact against the C oracle fed the device contribution log."""
+    if _ngpus() < G:
+        pytest.skip(f"needs {G} GPUs")
+    import torch
+
+    from paper_2005_00124_b200.driver import synthetic_grad
+    P, T, tau, n = 8, 12, 10, 25_559_081
+    port = 29950 + (hash((G, S, hier["WG_HIER"])) % 40)
+    env = dict(hier, WG_SPLIT_MIN_BYTES=str(8 << 20))
+    outs = _run(tmp_path, G, port, env_extra=env, P=P, S=S, T=T, tau=tau, nelem=n, dtype="f32", victims=1,
+                pipelined=1, save_grads=0, delay_us=300)
+    R = P // G
+    Wdev = np.stack([outs[r // R][f"W{r}"] for r in range(P)])
+    stamps = outs[0]["stamps"]
+    w0 = outs[0]["w0"]
+
+    def grad_fn(r, t):
+        return synthetic_grad(r, t, n, dtype=torch.float32, device="cuda").cpu().numpy()
+
+    want = _replay_streaming(P, S, tau, T, n, w0, grad_fn, stamps)
+    assert np.array_equal(Wdev, want)
+    late = sum(int((stamps[v] >= -1).sum() - (stamps[v] == v).sum()) for v in range(T) if (v + 1) % tau)
+    assert late > 0, "the injected straggler never contributed a stale model"
