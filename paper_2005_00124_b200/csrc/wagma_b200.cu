@@ -1645,9 +1645,12 @@ __device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename 
                         st_relaxed_sys(flag_base[j] + (int64_t(blockIdx.x) + (k0 + b) * gridDim.x) * kWarps + w,
                                        jb.version);
                 }
-                for (int e = lane; e < nk * NPa; e += 32) {  // the chunk's subtree partials
-                    const int pid = e % NPa, b = e / NPa;
-                    st_relaxed_sys(pflag_base[pid] + int64_t(blockIdx.x) + (k0 + b) * gridDim.x, p.part_version[pid]);
+                if constexpr (HIER) {
+                    for (int e = lane; e < nk * NPa; e += 32) {  // the chunk's subtree partials
+                        const int pid = e % NPa, b = e / NPa;
+                        st_relaxed_sys(pflag_base[pid] + int64_t(blockIdx.x) + (k0 + b) * gridDim.x,
+                                       p.part_version[pid]);
+                    }
                 }
             }
         }
