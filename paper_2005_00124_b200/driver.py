@@ -32,11 +32,12 @@ GradFn = Callable[[int, int], torch.Tensor]  # (rank, t) -> gradient on device
 
 def replay(opt: GroupAveragingOptimizer, grad_fn: GradFn, T: int, *,
            stamps: Optional[np.ndarray] = None, etas: Optional[np.ndarray] = None,
-           check_every: int = 0) -> None:
+           check_every: int = 0, on_step: Optional[Callable[[int], None]] = None) -> None:
     """Run iterations 0..T-1 for all local ranks, one launch per iteration.
 
     stamps[t, r] (optional) forces the contribution stamps of group version t
-    (alpha mode); etas[t, r] overrides the schedule's step size.
+    (alpha mode); etas[t, r] overrides the schedule's step size; on_step(t)
+    runs after iteration t is enqueued (e.g. `MetricsRecorder.record`).
     """
     ctx = opt.ctx
     ranks = list(ctx.local_ranks)
@@ -49,7 +50,10 @@ def replay(opt: GroupAveragingOptimizer, grad_fn: GradFn, T: int, *,
         forced = None
         if stamps is not None and opt.kind(t) == _lib.WG_JOB_STEP and opt.cfg.alpha:
             forced = {t: [int(s) for s in stamps[t]]}
+            opt.forced_log.update(forced)
         ctx.launch(jobs, forced=forced)
+        if on_step is not None:
+            on_step(t)
         if check_every and (t + 1) % check_every == 0:
             torch.cuda.current_stream(ctx.torch_device).synchronize()
             ctx.check()

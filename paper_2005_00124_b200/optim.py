@@ -134,6 +134,9 @@ class GroupAveragingOptimizer:
         self.ctx = ctx
         self.cfg = cfg
         self.T = cfg.T if T is None else T
+        # contribution stamps forced on replayed versions (the metrics
+        # recorder's staleness source when no descriptor was locked)
+        self.forced_log: dict[int, list[int]] = {}
         self.momentum = cfg.update_rule == "momentum"
         w0 = w0.to(device=ctx.torch_device, dtype=ctx.dtype).contiguous()
         self.W: dict[int, torch.Tensor] = {}
@@ -169,12 +172,16 @@ class GroupAveragingOptimizer:
         self.ctx.check_async()
         versions = {r: t for r in grads}
         forced = {t: forced_stamps} if forced_stamps is not None else None
+        if forced:
+            self.forced_log.update(forced)
         self.ctx.launch(self.jobs(versions, grads), forced=forced, stream=stream)
 
     def step_mixed(self, versions: Mapping[int, int], grads: Mapping[int, torch.Tensor],
                    forced: Optional[dict[int, list[int]]] = None, stream=None) -> None:
         """One launch in which ranks may be at different iterations (stragglers)."""
         self.ctx.check_async()
+        if forced:
+            self.forced_log.update(forced)
         self.ctx.launch(self.jobs(versions, grads), forced=forced, stream=stream)
 
     def statuses(self) -> list[JobStatus]:

@@ -20,6 +20,9 @@ the GPU box ever needs the reference:
                     gradients, the contribution log (rank, version, stamp)
                     captured from `optim._ContributionSink.append`
                     (`optim.py:310-319`), and the final weights.
+  metrics_*.npz     the reference's per-iteration `MetricsRecord` rows
+                    (`optim.py:218-234`) of three of those trajectories and
+                    the problem data their loss/gradient columns need.
 
 Usage:  python tests/golden/make_golden.py   (from the repo root)
 """
@@ -292,7 +295,26 @@ def record_training(name: str, P: int, opt, problem, delay, seed: int, mask_rule
                         grads=G, etas=E, stamps=stamps,
                         final=np.stack(res.final_weights),
                         meta=np.array(json.dumps(meta)))
+    if name in METRICS_CASES:
+        recs = res.records
+        prob = {"kind": problem.spec["kind"]}
+        if prob["kind"] == "quadratic":
+            arrays = {"eigs": problem.eigs, "x_star": problem.x_star}
+        else:
+            arrays = {"X": problem.X, "y": problem.y, "l2": np.array(problem.l2)}
+        np.savez_compressed(os.path.join(HERE, f"metrics_{name}.npz"),
+                            iteration=np.array([r.iteration for r in recs], dtype=np.int64),
+                            loss_mu=np.array([r.loss_mu for r in recs]),
+                            grad_norm_sq_mu=np.array([r.grad_norm_sq_mu for r in recs]),
+                            gamma=np.array([r.gamma for r in recs]),
+                            max_staleness=np.array([r.max_staleness for r in recs], dtype=np.int64),
+                            csv=np.array(ref_optim.CSV_HEADER + "\n" + "\n".join(r.csv_row() for r in recs)),
+                            problem=np.array(json.dumps(prob)), **arrays)
     return meta
+
+
+# trajectories whose metrics rows are pinned (tests/test_gpu_metrics.py)
+METRICS_CASES = ("logistic_p8s4_straggle", "quad_momentum_p8s2", "quad_s8_tau8")
 
 
 def make_training():

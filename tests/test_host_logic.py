@@ -110,3 +110,24 @@ def test_activation_message_counts_match_reference():
         assert sum(c["acts_sent"]) == P - 1
         assert c["activations_originated"] == [int(r == root) for r in range(P)]
         assert c["phases_sent"] == [S.bit_length() - 1] * P
+
+
+def test_metrics_csv_format_matches_reference():
+    """MetricsRecord.csv_row reproduces the reference's rows (optim.py:229-234)
+    byte for byte when given the reference's values (tests/golden/metrics_*.npz)."""
+    import glob
+    import os
+
+    import numpy as np
+
+    from conftest import GOLDEN
+    from paper_2005_00124_b200.metrics import CSV_HEADER, MetricsRecord
+
+    for path in sorted(glob.glob(os.path.join(GOLDEN, "metrics_*.npz"))):
+        lines = str(np.load(path)["csv"]).split("\n")
+        assert lines[0] == CSV_HEADER
+        for line in lines[1:]:
+            f = line.split(",")
+            rec = MetricsRecord(int(f[0]), float(f[1]), float(f[2]), float(f[3]), float(f[4]), int(f[5]),
+                                int(f[6]), int(f[7]))
+            assert rec.csv_row() == line
