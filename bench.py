@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--victims", type=int, default=0, help="StragglerPolicy victims per iteration")
     ap.add_argument("--extra-ms", type=float, default=0.0, help="extra delay of a victim rank's GPU")
     ap.add_argument("--straggler-seed", type=int, default=12)
+    ap.add_argument("--fixed-victim", type=int, default=-1,
+                    help="C4: this rank is the victim of every iteration (_FixedVictims, tests/test_optim.py:193-197)")
     ap.add_argument("--length-buckets", action="store_true",
                     help="C3: per-(rank, t) compute time base_ms * L / mean(L), L from WMT-style length buckets")
     return ap.parse_args()
@@ -324,6 +326,9 @@ def run_ours(a):
                           eta=EtaSchedule(value=0.1), update_rule="momentum", momentum=0.9)
     from paper_2005_00124_b200.straggler import StragglerPolicy
     policy = StragglerPolicy(a.victims, a.extra_ms, selection_seed=a.straggler_seed) if a.victims else None
+    if a.fixed_victim >= 0:
+        from paper_2005_00124_b200.straggler import FixedVictims
+        policy = FixedVictims(a.fixed_victim, a.extra_ms)
 
     from paper_2005_00124_b200.straggler import BucketedLengthDelay
     lengths = BucketedLengthDelay(a.base_ms, seed=a.straggler_seed) if a.length_buckets else None
@@ -492,7 +497,7 @@ def run_ours(a):
                 "group_avg_gbs": group_avg_gbs, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": gpu_launches, "clocks": clocks,
                 "replicas_after_sync": {"iteration": t - 1, "bit_identical": diag.identical, "gamma": diag.gamma}}
-        if a.blocking or a.victims or a.base_ms or a.length_buckets:
+        if a.blocking or a.victims or a.base_ms or a.length_buckets or a.fixed_victim >= 0:
             from paper_2005_00124_b200.optim import is_sync_iteration
             stale = total = 0
             for v in range(max(0, t - ctx.ring_depth + 1), t):
@@ -504,6 +509,7 @@ def run_ours(a):
                     stale += sum(1 for st in stamps if st != v)
             line["imbalance"] = {"activation": "blocking (beta)" if a.blocking else "wait-avoiding (alpha)",
                                  "base_ms": a.base_ms, "victims_per_iteration": a.victims, "extra_ms": a.extra_ms,
+                                 "fixed_victim": a.fixed_victim if a.fixed_victim >= 0 else None,
                                  "selection_seed": a.straggler_seed,
                                  "delay_model": "bucketed sequence lengths (WMT-style)" if a.length_buckets
                                  else "base + victims",

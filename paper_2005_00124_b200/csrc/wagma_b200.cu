@@ -138,6 +138,7 @@ struct LaunchParams {
     int32_t P, S, R, G, gpu_index, D, Dv, n_jobs, n_versions, n_plans, need_fence, pad;
     int64_t n, npad, n_tiles, tile_elems;
     int64_t grace_ns, timeout_ns, staleness_bound;
+    int32_t adaptive_grace, pad_ag;  // skip the grace wait for ranks late at the previous version
     int32_t job_of_rank[kMaxP];
     DevJob jobs[kMaxJobs];
     DevVersion versions[kMaxVersions];
@@ -440,18 +441,30 @@ __device__ void control_phase(const LaunchParams& p, int* s_activator) {
         }
         // Bounded grace window: ranks on other GPUs that join within it are
         // timely. Ranks on this GPU announced at launch start (final).
+        // Adaptive: a rank that was late for the previous version (a
+        // straggler) is not waited for, so a persistent straggler does not
+        // cost every version the whole window; it is still timely if it
+        // announces before the lock.
         const uint64_t t0 = globaltimer();
         const int q0 = lane, q1 = lane + 32;
+        bool skip0 = false, skip1 = false;
+        if (p.adaptive_grace && v >= 1) {
+            const Desc* dp = desc_ptr(p, v - 1);
+            if (ld_acquire_sys(&dp->state) == v * 4 + 2) {  // version v-1 locked (a live version)
+                skip0 = q0 < p.P && ld_relaxed_sys(&dp->stamps[q0]) < v - 1;
+                skip1 = q1 < p.P && ld_relaxed_sys(&dp->stamps[q1]) < v - 1;
+            }
+        }
         int64_t a0 = kNever, a1 = kNever;
         for (;;) {
             bool in = true;
             if (q0 < p.P) {
                 a0 = ld_acquire_sys(announce_ptr(p, q0));
-                if (a0 < v && q0 / p.R != p.gpu_index) in = false;
+                if (a0 < v && q0 / p.R != p.gpu_index && !skip0) in = false;
             }
             if (q1 < p.P) {
                 a1 = ld_acquire_sys(announce_ptr(p, q1));
-                if (a1 < v && q1 / p.R != p.gpu_index) in = false;
+                if (a1 < v && q1 / p.R != p.gpu_index && !skip1) in = false;
             }
             if (__all_sync(0xffffffffu, in)) break;
             if (globaltimer() - t0 > uint64_t(p.grace_ns)) break;
@@ -2737,6 +2750,7 @@ struct wg_ctx {
     int occ_split[2];
     int use_loc;              // single-GPU launches: TMA kernel (else the cp.async kernel)
     int use_hier;             // multi-GPU: exchange GPU-local subtree partials where the tree allows
+    int adaptive_grace;       // activator skips the grace wait for ranks late at the previous version
     int loc_dyn_max[2];       // dynamic shared memory available to wagma_local_kernel<T>
     int64_t* err_host;        // host-mapped mirror of the error word
     int64_t* err_host_dev;
@@ -2795,6 +2809,8 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     if (const char* lc = getenv("WG_LOC")) ctx->use_loc = atoi(lc);
     ctx->use_hier = 1;
     if (const char* hh = getenv("WG_HIER")) ctx->use_hier = atoi(hh);
+    ctx->adaptive_grace = 1;
+    if (const char* ag = getenv("WG_ADAPTIVE_GRACE")) ctx->adaptive_grace = atoi(ag);
     ctx->fence_scope = 1;  // GPU scope for per-tile flags (see publish_tile)
     if (const char* fs = getenv("WG_FENCE_SCOPE")) {
         if (!strcmp(fs, "sys")) ctx->fence_scope = 0;
@@ -3109,6 +3125,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
     p.n_tiles = ctx->n_tiles;
     p.tile_elems = ctx->tile_elems;
     p.grace_ns = c.grace_ns;
+    p.adaptive_grace = ctx->adaptive_grace;
     p.timeout_ns = c.timeout_ns;
     p.staleness_bound = c.staleness_bound;
     p.status = ctx->status_dev;

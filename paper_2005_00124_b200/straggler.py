@@ -15,7 +15,7 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["StragglerPolicy", "DelayModel", "compute_delay", "BucketedLengthDelay", "WMT_BUCKETS"]
+__all__ = ["StragglerPolicy", "FixedVictims", "DelayModel", "compute_delay", "BucketedLengthDelay", "WMT_BUCKETS"]
 
 
 @dataclass(frozen=True)
@@ -34,6 +34,20 @@ class StragglerPolicy:
         rng = np.random.default_rng([self.selection_seed, iteration])
         picks = rng.choice(P, size=self.victims_per_iteration, replace=False)
         return frozenset(int(v) for v in picks)
+
+
+class FixedVictims(StragglerPolicy):
+    """One fixed victim rank every iteration (the reference tests' `_FixedVictims`,
+    tests/test_optim.py:193-197): C4's injected straggler."""
+
+    def __init__(self, rank: int, extra_delay_ms: float):
+        super().__init__(1, extra_delay_ms, 0)
+        object.__setattr__(self, "rank", int(rank))
+
+    def victims(self, iteration: int, P: int) -> frozenset[int]:
+        if not 0 <= self.rank < P:
+            raise ValueError(f"victim rank {self.rank} outside 0..{P - 1}")
+        return frozenset({self.rank})
 
 
 @dataclass(frozen=True)

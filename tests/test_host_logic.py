@@ -131,3 +131,15 @@ def test_metrics_csv_format_matches_reference():
             rec = MetricsRecord(int(f[0]), float(f[1]), float(f[2]), float(f[3]), float(f[4]), int(f[5]),
                                 int(f[6]), int(f[7]))
             assert rec.csv_row() == line
+
+
+def test_fixed_victims_policy():
+    """C4's fixed straggler (tests/test_optim.py:193-197 `_FixedVictims`)."""
+    import pytest
+
+    from paper_2005_00124_b200.straggler import FixedVictims
+    pol = FixedVictims(1, 5.0)
+    assert all(pol.victims(t, 4) == frozenset({1}) for t in range(20))
+    assert pol.extra_delay_ms == 5.0
+    with pytest.raises(ValueError):
+        FixedVictims(4, 1.0).victims(0, 4)
