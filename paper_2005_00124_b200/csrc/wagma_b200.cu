@@ -155,6 +155,8 @@ struct LaunchParams {
     int32_t red_warps;    // split kernel: stream-A reducer warps (4 or 8 of the 12 shared with stream B)
     int32_t loc_stages;   // single-GPU TMA kernel: input-ring stages
     int64_t* err_host;    // host-mapped mirror of the error word (wg_ctx_error_async)
+    int32_t mg_cap_a, mg_cap_b;  // wagma_mg_kernel: phase-1 / phase-2 row capacity (chunk rows)
+    int32_t mg_split, pad_mg;    // wagma_mg_kernel: split (reduce-scatter) partial sums where they pay
     // hierarchical sums (multi-GPU pull kernel): a plan whose lowest plan_hl
     // tree levels stay inside one GPU exchanges GPU-local subtree partials
     // instead of leaves when all its members are timely
@@ -1250,7 +1252,7 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 #define WG_LOC_TILES 2
 #endif
 #ifndef WG_LOC_CONSUMER_WARPS
-#define WG_LOC_CONSUMER_WARPS 8
+#define WG_LOC_CONSUMER_WARPS 16
 #endif
 #ifndef WG_LOC_EVICT_FIRST  // L2 evict-first policy on the TMA input loads (measured +1%)
 #define WG_LOC_EVICT_FIRST 1
@@ -1264,6 +1266,7 @@ constexpr int kLocThreads = kLocConsumers + 64;            // + producer warp + 
 constexpr int kLocChunkVecs = kLocTiles * kThreads;        // 16-byte vectors per row of a stage
 constexpr int kLocVPT = kLocChunkVecs / kLocConsumers;     // vectors per consumer thread per item
 constexpr int kLocMaxStages = 16;
+constexpr int kMgMaxStagesA = 16, kMgMaxStagesB = 16;
 static_assert(kLocChunkVecs % kLocConsumers == 0, "a chunk row must split evenly over the consumers");
 
 // Per-job constants of the single-GPU kernel, staged in shared memory once
@@ -1540,6 +1543,545 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
         my_tiles += unsigned(p.n_tiles - c * kLocTiles < kLocTiles ? p.n_tiles - c * kLocTiles : kLocTiles);
     __syncthreads();
     if (ready != 1) sm.abort = 1;
+    publish_slots(p, sm.abort ? 0u : my_tiles);
+    if (blockIdx.x == 0) {
+        __syncthreads();
+        const bool res = ready == 1;
+        if (tid < p.n_jobs) {
+            const DevJob& jb = p.jobs[tid];
+            wg_job_status stt;
+            stt.version = jb.version;
+            stt.contrib_stamp = (jb.kind == WG_JOB_LOCAL_STEP || !res) ? jb.version : sm.stamps[jb.vidx][jb.rank];
+            stt.timely = stt.contrib_stamp == jb.version;
+            stt.root = activation_root(p, jb, res);
+            stt.activator = jb.vidx >= 0 && sm.activator[jb.vidx] && stt.root == jb.rank;
+            stt.error = int32_t(ld_relaxed_sys(err_ptr(p)));
+            p.status[tid] = stt;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU kernel with hierarchical sums on the TMA produce path
+//
+// The single-GPU kernel's produce side (TMA input ring, consumer warps
+// computing W' from shared memory) plus the exchange, chunk by chunk:
+//  - produce(c): W' of every job (m and send-ring stores), this GPU's
+//    subtree partials (butterfly order) stored for the peers, then one fence
+//    and the chunk's readiness flags (leaf flags of every produced rank,
+//    partial flags);
+//  - phase 1 (chunk c - kMgLag1): plans summed here -- leaf pull, partial
+//    pull, or the chunks this GPU owns of a split (reduce-scatter) plan,
+//    whose reduced chunk is stored and flagged for the other members;
+//  - phase 2 (chunk c - kMgLag2): split plans owned elsewhere: the owner's
+//    reduced chunk. Phase 1 never waits on another GPU's phase 1 or 2, so
+//    no wait cycle exists.
+// Warp 0 streams the inputs by TMA; warp 1 runs the activation protocol,
+// resolves every plan's effective leaves (partials when all members are
+// timely) and streams phase-1 rows (peers' partials/leaves over NVLink,
+// this GPU's from L2); warp 2 streams phase-2 rows (owners' reduced
+// chunks). The consumers never poll a flag.
+// ---------------------------------------------------------------------------
+
+#ifndef WG_MG_LAG1
+#define WG_MG_LAG1 2
+#endif
+#ifndef WG_MG_LAG2
+#define WG_MG_LAG2 4
+#endif
+#ifndef WG_MG_IN_STAGES
+#define WG_MG_IN_STAGES 3
+#endif
+constexpr int kMgLag1 = WG_MG_LAG1, kMgLag2 = WG_MG_LAG2;
+constexpr int kMgThreads = kLocConsumers + 96;  // + input producer, control/phase-1 puller, phase-2 puller
+constexpr int kMgMaxEff = 16;                   // effective leaves per plan
+enum MgMode : int8_t { kMgPull = 0, kMgHier = 1, kMgSplit = 2 };
+
+template <typename T>
+__global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_constant__ LaunchParams p) {
+    using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
+    extern __shared__ __align__(128) unsigned char dyn_smem[];
+    __shared__ SmemCtl sm;
+    __shared__ LocJob<T> s_job[kMaxJobs];
+    __shared__ __align__(8) uint64_t fin[kLocMaxStages], ein[kLocMaxStages];     // input ring
+    __shared__ __align__(8) uint64_t fa[kMgMaxStagesA], ea[kMgMaxStagesA];       // phase-1 rows
+    __shared__ __align__(8) uint64_t fb[kMgMaxStagesB], eb[kMgMaxStagesB];       // phase-2 rows
+    __shared__ volatile int ready;
+    __shared__ int s_nsa, s_nsb, s_rows_a, s_rows_b;
+    // local partials: buffers, flags and their leaf jobs in leaf order
+    __shared__ T* s_part[kMaxJobs];
+    __shared__ int64_t* s_pflag[kMaxJobs];
+    __shared__ int8_t s_pjob[kMaxJobs][16];
+    __shared__ int8_t s_plog[kMaxJobs];
+    // per plan, after lock-in: mode, effective leaves (sources and flags)
+    __shared__ int8_t s_mode[kMaxPlans], s_elog[kMaxPlans], s_ne[kMaxPlans];
+    __shared__ const T* s_esrc[kMaxPlans][kMgMaxEff];       // effective leaf buffers (tile 0)
+    __shared__ const int64_t* s_eflag[kMaxPlans][kMgMaxEff];  // their flags (tile 0)
+    __shared__ int8_t s_estride[kMaxPlans][kMgMaxEff];      // flag words per tile (kWarps: leaf, 1: partial)
+    __shared__ int64_t s_ewant[kMaxPlans][kMgMaxEff];
+    __shared__ T* s_red[kMaxPlans][kMgMaxEff];              // split: reduced-chunk buffer of owner u
+    __shared__ int64_t* s_redflag[kMaxPlans][kMgMaxEff];
+    __shared__ int8_t s_ownlocal[kMaxPlans][kMgMaxEff];
+    __shared__ int64_t s_ver[kMaxPlans];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int J = p.n_jobs, NSI = p.loc_stages, NP = p.n_plans;
+    constexpr int C = kLocChunkVecs;
+    const int64_t chunk_elems = int64_t(C) * E;
+    const int64_t n_chunks = (p.n_tiles + kLocTiles - 1) / kLocTiles;
+    const int64_t my_nchunks = blockIdx.x < n_chunks ? (n_chunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    V* rows_in = reinterpret_cast<V*>(dyn_smem);              // [NSI][3][C]
+    V* wst = rows_in + size_t(NSI) * 3 * C;                   // [J][C]
+    V* rows_a = wst + size_t(J) * C;                          // [mg_cap_a][C]
+    V* rows_b = rows_a + size_t(p.mg_cap_a) * C;              // [mg_cap_b][C]
+    if (tid == 0) {
+        sm.abort = 0;
+        ready = 0;
+        for (int st = 0; st < NSI; ++st) {
+            mbar_init(&fin[st], 1);
+            mbar_init(&ein[st], kLocConsumers / 32);
+        }
+        for (int st = 0; st < kMgMaxStagesA; ++st) {
+            mbar_init(&fa[st], 1);
+            mbar_init(&ea[st], kLocConsumers / 32);
+        }
+        for (int st = 0; st < kMgMaxStagesB; ++st) {
+            mbar_init(&fb[st], 1);
+            mbar_init(&eb[st], kLocConsumers / 32);
+        }
+        for (int k = 0; k < J; ++k) {  // the producers' job order -> partial leaf lists
+            const int pid = p.job_part[k];
+            if (pid >= 0) {
+                s_pjob[pid][p.job_ppos[k]] = p.job_order[k];
+                if (p.job_plast[k]) s_plog[pid] = int8_t(31 - __clz(p.job_ppos[k] + 1));
+            }
+        }
+    }
+    if (tid < kMaxVersions) sm.activator[tid] = 0;
+    if (tid < J) {
+        const DevJob& jb = p.jobs[tid];
+        LocJob<T> lj;
+        lj.W = static_cast<T*>(jb.W);
+        lj.m = static_cast<T*>(jb.m);
+        lj.g = static_cast<const T*>(jb.g);
+        lj.fresh = static_cast<const T*>(jb.fresh);
+        lj.ring = jb.produces ? ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) : nullptr;
+        lj.eta = T(jb.eta);
+        lj.beta = T(jb.beta);
+        lj.kind = jb.kind;
+        lj.mom = jb.update_rule == WG_UPDATE_MOMENTUM;
+        s_job[tid] = lj;
+    }
+    if (tid < p.n_parts) {
+        s_part[tid] = part_ptr<T>(p, p.part_key[tid], p.part_version[tid]);
+        s_pflag[tid] = part_flag_ptr(p, p.part_key[tid], 0);
+    }
+    __syncthreads();
+    const unsigned chunk_bytes_full = unsigned(C) * 16u;
+    // padded buffers (send ring, partials, reduced chunks): bytes of chunk kc
+    auto pad_bytes = [&](int64_t c) -> unsigned {
+        const int64_t t0 = c * kLocTiles;
+        const int64_t nt = p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles;
+        return unsigned(nt * p.tile_elems * int64_t(sizeof(T)));
+    };
+    // owner (effective-leaf index) of chunk kc of a split plan
+    auto owner = [&](int pl, int64_t kc) -> int { return int(kc % s_ne[pl]); };
+    // phase-1 / phase-2 rows of CTA-local chunk kc (identical in pullers and consumers)
+    auto rows_of = [&](int64_t kc, int& ra, int& rb) {
+        ra = rb = 0;
+        for (int pl = 0; pl < NP; ++pl) {
+            if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, kc)])
+                ra += s_ne[pl];
+            else
+                rb += 1;
+        }
+    };
+    // wait for flags >= want of one effective source over the chunk's tiles
+    auto poll = [&](const int64_t* f0, int stride, int64_t want, int64_t c) -> int {
+        if (want == kNever) return 0;  // a completed older slot (checked at resolve)
+        const int64_t t0 = c * kLocTiles;
+        const int64_t nt = p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles;
+        for (int64_t t = t0; t < t0 + nt; ++t)
+            for (int w = 0; w < stride; ++w) {
+                const int64_t* f = f0 + t * stride + w;
+                const uint64_t tt = globaltimer();
+                int it = 0;
+                int64_t v = ld_relaxed_sys(f);
+                while (v < want) {
+                    if ((++it & 63) == 0 && (globaltimer() - tt > uint64_t(p.timeout_ns) || aborted(p))) return WG_ETIMEOUT;
+                    __nanosleep(32);
+                    v = ld_relaxed_sys(f);
+                }
+                if (v >= want + p.D) return WG_EPROTO;
+            }
+        return 0;
+    };
+    auto acquire_for_tma = [&]() {
+        if (p.fence_scope == 0)
+            fence_sys();
+        else
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    };
+
+    if (warp == 0) {
+        // ---------------- input producer (TMA) ----------------
+        if (lane == 0) {
+            const uint64_t pol = WG_LOC_EVICT_FIRST ? policy_evict_first() : 0;
+            auto load = [&](void* d, const T* src, unsigned nb, uint64_t* bar) {
+                if (WG_LOC_EVICT_FIRST)
+                    bulk_g2s_hint(d, src, nb, bar, pol);
+                else
+                    bulk_g2s(d, src, nb, bar);
+            };
+            int st = 0;
+            unsigned ph = 0;
+            int64_t k = 0;
+            bool ok = true;
+            for (int64_t c = blockIdx.x; c < n_chunks && ok; c += gridDim.x) {
+                const int64_t e0 = c * chunk_elems;
+                const int64_t rem = (p.n - e0) * int64_t(sizeof(T));
+                const unsigned bytes = rem >= chunk_bytes_full ? chunk_bytes_full : (rem > 0 ? unsigned(rem) & ~15u : 0u);
+                for (int jj = 0; jj < J; ++jj, ++k) {
+                    const int j = p.job_order[jj];
+                    if (k >= NSI && !mbar_wait(p, &ein[st], ph ^ 1u)) {
+                        ok = false;
+                        break;
+                    }
+                    const LocJob<T>& jb = s_job[j];
+                    V* dst = rows_in + size_t(st) * 3 * C;
+                    if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
+                        mbar_arrive_expect_tx(&fin[st], bytes);
+                        if (bytes) load(dst, jb.fresh + e0, bytes, &fin[st]);
+                    } else {
+                        mbar_arrive_expect_tx(&fin[st], (jb.mom ? 3u : 2u) * bytes);
+                        if (bytes) {
+                            load(dst, jb.W + e0, bytes, &fin[st]);
+                            load(dst + C, jb.g + e0, bytes, &fin[st]);
+                            if (jb.mom) load(dst + 2 * C, jb.m + e0, bytes, &fin[st]);
+                        }
+                    }
+                    if (++st == NSI) st = 0, ph ^= 1u;
+                }
+            }
+            if (!ok) {
+                raise_error(p, WG_ETIMEOUT, k);
+                sm.abort = 1;
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- control + phase-1 puller ----------------
+        if (blockIdx.x == 0) control_phase(p, sm.activator);
+        bool res = resolve_core<T>(p, sm, lane, 32, [] { __syncwarp(); });
+        if (res && lane == 0) {
+            int ra_max = 0, rb_max = 0;
+            for (int pl = 0; pl < NP; ++pl) {
+                const DevPlan& P_ = p.plans[pl];
+                const int64_t v = p.versions[P_.vidx].version;
+                s_ver[pl] = v;
+                bool hier = p.plan_hl[pl] > 0;
+                for (int li = 0; li < P_.n_leaves && hier; ++li) hier = sm.stamps[P_.vidx][P_.leaves[li]] == v;
+                if (hier) {
+                    const int hl = p.plan_hl[pl];
+                    const int ne = P_.n_leaves >> hl;
+                    unsigned gpus = 0;
+                    for (int u = 0; u < ne; ++u) {
+                        const int key = P_.leaves[u << hl];
+                        gpus |= 1u << (key / p.R);
+                        s_esrc[pl][u] = part_ptr<T>(p, key, v);
+                        s_eflag[pl][u] = part_flag_ptr(p, key, 0);
+                        s_estride[pl][u] = 1;
+                        s_ewant[pl][u] = v;
+                        s_red[pl][u] = red_ptr<T>(p, key, v);
+                        s_redflag[pl][u] = red_flag_ptr(p, key, 0);
+                        s_ownlocal[pl][u] = int8_t(key / p.R == p.gpu_index);
+                    }
+                    s_ne[pl] = int8_t(ne);
+                    s_elog[pl] = int8_t(P_.log_leaves - hl);
+                    s_mode[pl] = (p.mg_split && split_pays(ne, __popc(gpus))) ? kMgSplit : kMgHier;
+                } else {
+                    // leaf pull (a member is stale): every leaf's send slot
+                    for (int li = 0; li < P_.n_leaves; ++li) {
+                        const int q = P_.leaves[li];
+                        const int64_t st = sm.stamps[P_.vidx][q];
+                        s_esrc[pl][li] = ring_ptr<T>(p, q, slot_of(p, st));
+                        s_eflag[pl][li] = flag_ptr(p, q, 0, 0);
+                        s_estride[pl][li] = kWarps;
+                        s_ewant[pl][li] = sm.leaf_src[pl][li] == kSrcReady ? kNever : st;
+                        s_ownlocal[pl][li] = 1;
+                    }
+                    s_ne[pl] = int8_t(P_.n_leaves);
+                    s_elog[pl] = int8_t(P_.log_leaves);
+                    s_mode[pl] = kMgPull;
+                }
+                ra_max += s_ne[pl];
+                rb_max += s_mode[pl] == kMgSplit;
+            }
+            s_rows_a = ra_max;
+            s_rows_b = rb_max;
+            s_nsa = ra_max ? (p.mg_cap_a / ra_max < kMgMaxStagesA ? p.mg_cap_a / ra_max : kMgMaxStagesA) : kMgMaxStagesA;
+            s_nsb = rb_max ? (p.mg_cap_b / rb_max < kMgMaxStagesB ? p.mg_cap_b / rb_max : kMgMaxStagesB) : kMgMaxStagesB;
+            if (s_nsa < 1 || s_nsb < 1) {
+                raise_error(p, WG_EINVAL, ra_max);
+                res = false;
+            }
+        }
+        res = __shfl_sync(0xffffffffu, res, 0);
+        if (lane == 0) {
+            __threadfence_block();
+            ready = res ? 1 : 2;
+        }
+        __syncwarp();
+        const int NSA = s_nsa;
+        int st = 0;
+        unsigned ph = 0;
+        int64_t k = 0;
+        for (int64_t kc = 0; res && kc < my_nchunks; ++kc) {
+            int ra, rb;
+            rows_of(kc, ra, rb);
+            if (!ra) continue;
+            const int64_t c = int64_t(blockIdx.x) + kc * gridDim.x;
+            if (k >= NSA && !mbar_wait(p, &ea[st], ph ^ 1u)) {
+                if (lane == 0) raise_error(p, WG_ETIMEOUT, kc);
+                break;
+            }
+            // wait for every source of the chunk (lane e polls source e), then copy
+            int rc = 0, e = 0;
+            for (int pl = 0; pl < NP; ++pl) {
+                if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, kc)]) continue;
+                for (int u = 0; u < s_ne[pl]; ++u, ++e)
+                    if ((e & 31) == lane && !rc) rc = poll(s_eflag[pl][u], s_estride[pl][u], s_ewant[pl][u], c);
+            }
+            if (rc) raise_error(p, rc, kc);
+            if (__any_sync(0xffffffffu, rc != 0)) break;
+            acquire_for_tma();
+            const unsigned cb = pad_bytes(c);
+            if (lane == 0) mbar_arrive_expect_tx(&fa[st], unsigned(ra) * cb);
+            __syncwarp();
+            e = 0;
+            for (int pl = 0; pl < NP; ++pl) {
+                if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, kc)]) continue;
+                for (int u = 0; u < s_ne[pl]; ++u, ++e)
+                    if ((e & 31) == lane)
+                        bulk_g2s(rows_a + (size_t(st) * s_rows_a + e) * C, s_esrc[pl][u] + c * chunk_elems, cb, &fa[st]);
+            }
+            __syncwarp();
+            if (++st == NSA) st = 0, ph ^= 1u;
+            ++k;
+        }
+    } else if (warp == 2) {
+        // ---------------- phase-2 puller: owners' reduced chunks ----------------
+        while (ready == 0) __nanosleep(64);
+        __threadfence_block();
+        if (ready == 1 && s_rows_b) {
+            const int NSB = s_nsb;
+            int st = 0;
+            unsigned ph = 0;
+            int64_t k = 0;
+            for (int64_t kc = 0; kc < my_nchunks; ++kc) {
+                int ra, rb;
+                rows_of(kc, ra, rb);
+                if (!rb) continue;
+                const int64_t c = int64_t(blockIdx.x) + kc * gridDim.x;
+                if (k >= NSB && !mbar_wait(p, &eb[st], ph ^ 1u)) {
+                    if (lane == 0) raise_error(p, WG_ETIMEOUT, kc);
+                    break;
+                }
+                int rc = 0, e = 0;
+                for (int pl = 0; pl < NP; ++pl) {
+                    if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, kc)]) continue;
+                    if ((e & 31) == lane) rc = poll(s_redflag[pl][owner(pl, kc)], 1, s_ver[pl], c);
+                    ++e;
+                }
+                if (rc) raise_error(p, rc, kc);
+                if (__any_sync(0xffffffffu, rc != 0)) break;
+                acquire_for_tma();
+                const unsigned cb = pad_bytes(c);
+                if (lane == 0) mbar_arrive_expect_tx(&fb[st], unsigned(rb) * cb);
+                __syncwarp();
+                e = 0;
+                for (int pl = 0; pl < NP; ++pl) {
+                    if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, kc)]) continue;
+                    if ((e & 31) == lane)
+                        bulk_g2s(rows_b + (size_t(st) * s_rows_b + e) * C, s_red[pl][owner(pl, kc)] + c * chunk_elems,
+                                 cb, &fb[st]);
+                    ++e;
+                }
+                __syncwarp();
+                if (++st == NSB) st = 0, ph ^= 1u;
+                ++k;
+            }
+        }
+    } else {
+        // ---------------- consumers ----------------
+        const int ct = tid - 96;
+        const int cw = ct >> 5;
+        unsigned bad = 0;
+        int sti = 0, sta = 0, stb = 0;
+        unsigned phi = 0, pha = 0, phb = 0;
+        int64_t ka = 0, kb = 0;
+        bool ok = true, resolved = false;
+        // consumers-only named barrier (id 1)
+        auto cbar = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(kLocConsumers) : "memory"); };
+        auto fence_pub = [&]() {
+            if (p.fence_scope == 0)
+                fence_sys();
+            else if (p.fence_scope == 1)
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        };
+        for (int64_t i = 0; ok && i < my_nchunks + kMgLag2; ++i) {
+            if (i < my_nchunks) {
+                // ---- produce chunk i ----
+                const int64_t c = int64_t(blockIdx.x) + i * gridDim.x;
+                const int64_t e0 = c * chunk_elems;
+                const bool fullc = e0 + chunk_elems <= p.n;
+                for (int jj = 0; jj < J; ++jj) {
+                    const int j = p.job_order[jj];
+                    if (!mbar_wait(p, &fin[sti], phi)) {
+                        ok = false;
+                        break;
+                    }
+                    const V* r = rows_in + size_t(sti) * 3 * C;
+                    if (fullc)
+                        bad |= loc_item<T, true>(p, s_job[j], j, e0, r, wst, ct);
+                    else
+                        bad |= loc_item<T, false>(p, s_job[j], j, e0, r, wst, ct);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&ein[sti]);
+                    if (++sti == NSI) sti = 0, phi ^= 1u;
+                }
+                if (!ok) break;
+                // this GPU's subtree partials (butterfly order inside the subtree)
+                for (int pid = 0; pid < p.n_parts; ++pid) {
+#pragma unroll
+                    for (int kv = 0; kv < kLocVPT; ++kv) {
+                        const int v = kv * kLocConsumers + ct;
+                        const int64_t idx = e0 + int64_t(v) * E;
+                        if (idx >= p.npad) continue;
+                        auto fetch = [&](int leaf) -> V { return wst[s_pjob[pid][leaf] * C + v]; };
+                        __stcg(reinterpret_cast<V*>(s_part[pid] + idx), tree_sum<T>(fetch, s_plog[pid]));
+                    }
+                }
+                // publish: every consumer's stores, one fence, the chunk's flags
+                cbar();
+                if (cw == 0) {
+                    if (lane == 0) fence_pub();
+                    __syncwarp();
+                    const int64_t t0 = c * kLocTiles;
+                    const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
+                    for (int e = lane; e < J * nt * kWarps; e += 32) {
+                        const int w = e % kWarps, tt = (e / kWarps) % nt, j = e / (kWarps * nt);
+                        const DevJob& jb = p.jobs[j];
+                        if (jb.produces) st_relaxed_sys(flag_ptr(p, jb.rank, t0 + tt, w), jb.version);
+                    }
+                    for (int e = lane; e < p.n_parts * nt; e += 32)
+                        st_relaxed_sys(s_pflag[e / nt] + t0 + e % nt, p.part_version[e / nt]);
+                }
+            }
+            if (!resolved && i >= kMgLag1) {
+                while (ready == 0) __nanosleep(32);
+                __threadfence_block();
+                if (ready != 1) break;
+                resolved = true;
+            }
+            const int64_t x1 = i - kMgLag1;
+            if (x1 >= 0 && x1 < my_nchunks) {
+                // ---- phase 1 of chunk x1 ----
+                const int64_t c = int64_t(blockIdx.x) + x1 * gridDim.x;
+                const int64_t e0 = c * chunk_elems;
+                int ra, rb;
+                rows_of(x1, ra, rb);
+                if (ra) {
+                    if (!mbar_wait(p, &fa[sta], pha)) {
+                        ok = false;
+                        break;
+                    }
+                    const V* lb = rows_a + size_t(sta) * s_rows_a * C;
+                    bool owned = false;
+                    int e = 0;
+                    for (int pl = 0; pl < NP; ++pl) {
+                        if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, x1)]) continue;
+                        const DevPlan& P_ = p.plans[pl];
+#pragma unroll
+                        for (int kv = 0; kv < kLocVPT; ++kv) {
+                            const int v = kv * kLocConsumers + ct;
+                            const int64_t idx = e0 + int64_t(v) * E;
+                            if (idx >= p.npad) continue;
+                            auto fetch = [&](int leaf) -> V { return lb[(e + leaf) * C + v]; };
+                            const V acc = tree_sum<T>(fetch, s_elog[pl]);
+                            if (s_mode[pl] == kMgSplit)  // the owner's reduced chunk, for the other members
+                                __stcg(reinterpret_cast<V*>(s_red[pl][owner(pl, x1)] + idx), acc);
+                            finish_members<T>(p, sm, P_, acc, idx, [&](int j) {
+                                return __ldcg(reinterpret_cast<const V*>(s_job[j].ring + idx));
+                            });
+                        }
+                        owned = owned || s_mode[pl] == kMgSplit;
+                        e += s_ne[pl];
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&ea[sta]);
+                    if (++sta == s_nsa) sta = 0, pha ^= 1u;
+                    ++ka;
+                    if (owned) {
+                        cbar();
+                        if (cw == 0) {
+                            if (lane == 0) fence_pub();
+                            __syncwarp();
+                            const int64_t t0 = c * kLocTiles;
+                            const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
+                            for (int pl = 0; pl < NP; ++pl)
+                                if (s_mode[pl] == kMgSplit && s_ownlocal[pl][owner(pl, x1)] && lane < nt)
+                                    st_relaxed_sys(s_redflag[pl][owner(pl, x1)] + t0 + lane, s_ver[pl]);
+                        }
+                    }
+                }
+            }
+            const int64_t x2 = i - kMgLag2;
+            if (x2 >= 0 && x2 < my_nchunks) {
+                // ---- phase 2 of chunk x2: reduced chunks owned elsewhere ----
+                const int64_t c = int64_t(blockIdx.x) + x2 * gridDim.x;
+                const int64_t e0 = c * chunk_elems;
+                int ra, rb;
+                rows_of(x2, ra, rb);
+                if (rb) {
+                    if (!mbar_wait(p, &fb[stb], phb)) {
+                        ok = false;
+                        break;
+                    }
+                    const V* lb = rows_b + size_t(stb) * s_rows_b * C;
+                    int e = 0;
+                    for (int pl = 0; pl < NP; ++pl) {
+                        if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, x2)]) continue;
+                        const DevPlan& P_ = p.plans[pl];
+#pragma unroll
+                        for (int kv = 0; kv < kLocVPT; ++kv) {
+                            const int v = kv * kLocConsumers + ct;
+                            const int64_t idx = e0 + int64_t(v) * E;
+                            if (idx >= p.npad) continue;
+                            finish_members<T>(p, sm, P_, lb[e * C + v], idx, [&](int j) {
+                                return __ldcg(reinterpret_cast<const V*>(s_job[j].ring + idx));
+                            });
+                        }
+                        ++e;
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&eb[stb]);
+                    if (++stb == s_nsb) stb = 0, phb ^= 1u;
+                    ++kb;
+                }
+            }
+        }
+        if (!ok) {
+            if (lane == 0) raise_error(p, WG_ETIMEOUT, blockIdx.x);
+            sm.abort = 1;
+        }
+        report_divergence(p, bad);
+    }
+    unsigned my_tiles = 0;
+    for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x)
+        my_tiles += unsigned(p.n_tiles - c * kLocTiles < kLocTiles ? p.n_tiles - c * kLocTiles : kLocTiles);
+    __syncthreads();
+    if (ready != 1 || aborted(p)) sm.abort = 1;
     publish_slots(p, sm.abort ? 0u : my_tiles);
     if (blockIdx.x == 0) {
         __syncthreads();
@@ -2717,6 +3259,7 @@ struct Blob {
     // multi-GPU kernel runs (only the split kernel publishes reduced tiles),
     // its tile ownership (grid = SMs x occupancy) and the flag fence scope
     int32_t use_nvl, use_split, split_span, fence_scope, sms, occ_split, occ_nvl, use_hier;
+    int32_t use_mg, pad_b;
     int64_t split_min_bytes;
     cudaIpcMemHandle_t handle;
 };
@@ -2750,6 +3293,8 @@ struct wg_ctx {
     int occ_split[2];
     int use_loc;              // single-GPU launches: TMA kernel (else the cp.async kernel)
     int use_hier;             // multi-GPU: exchange GPU-local subtree partials where the tree allows
+    int use_mg;               // hierarchical launches: the TMA-produce multi-GPU kernel (else the pull kernel)
+    int mg_dyn_max[2];        // dynamic shared memory available to wagma_mg_kernel<T>
     int adaptive_grace;       // activator skips the grace wait for ranks late at the previous version
     int loc_dyn_max[2];       // dynamic shared memory available to wagma_local_kernel<T>
     int64_t* err_host;        // host-mapped mirror of the error word
@@ -2809,6 +3354,8 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     if (const char* lc = getenv("WG_LOC")) ctx->use_loc = atoi(lc);
     ctx->use_hier = 1;
     if (const char* hh = getenv("WG_HIER")) ctx->use_hier = atoi(hh);
+    ctx->use_mg = 1;
+    if (const char* mg = getenv("WG_MG")) ctx->use_mg = atoi(mg);
     ctx->adaptive_grace = 1;
     if (const char* ag = getenv("WG_ADAPTIVE_GRACE")) ctx->adaptive_grace = atoi(ag);
     ctx->fence_scope = 1;  // GPU scope for per-tile flags (see publish_tile)
@@ -2842,7 +3389,8 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     off = align_up(off + int64_t(ctx->R) * ctx->n_tiles * kWarps * 8, 4096);
     L.ring = off;
     off = align_up(off + int64_t(ctx->R) * ctx->D * ctx->npad * int64_t(ctx->esize), 4096);
-    const int64_t red = (ctx->use_split && c.n_gpus >= ctx->split_span && c.P <= kSplitMaxP) ? 1 : 0;
+    const int64_t red = ((ctx->use_split && c.n_gpus >= ctx->split_span && c.P <= kSplitMaxP) ||
+                         (ctx->use_hier && ctx->use_split && c.n_gpus >= 2)) ? 1 : 0;
     L.red_flags = off;
     off = align_up(off + red * int64_t(ctx->R) * ctx->n_tiles * 8, 4096);
     L.red_ring = off;
@@ -2901,6 +3449,14 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
             cudaFuncAttributes fa[2];
             if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa[0], wagma_local_kernel<float>);
             if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa[1], wagma_local_kernel<double>);
+            cudaFuncAttributes fm[2];
+            if (e == cudaSuccess) e = cudaFuncGetAttributes(&fm[0], wagma_mg_kernel<float>);
+            if (e == cudaSuccess) e = cudaFuncGetAttributes(&fm[1], wagma_mg_kernel<double>);
+            for (int di = 0; di < 2 && e == cudaSuccess; ++di) {
+                ctx->mg_dyn_max[di] = optin - int(fm[di].sharedSizeBytes) - 1024;
+                e = cudaFuncSetAttribute(di == 0 ? (const void*)wagma_mg_kernel<float> : (const void*)wagma_mg_kernel<double>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->mg_dyn_max[di]);
+            }
             for (int di = 0; di < 2 && e == cudaSuccess; ++di) {
                 ctx->loc_dyn_max[di] = optin - int(fa[di].sharedSizeBytes) - 1024;
                 e = cudaFuncSetAttribute(di == 0 ? (const void*)wagma_local_kernel<float> : (const void*)wagma_local_kernel<double>,
@@ -2977,6 +3533,7 @@ int wg_ctx_export(wg_ctx* ctx, void* blob, size_t cap, size_t* len) {
     b.occ_nvl = ctx->occ_nvl[ctx->cfg.dtype == WG_F32 ? 0 : 1];
     b.split_min_bytes = ctx->split_min_bytes;
     b.use_hier = ctx->use_hier;
+    b.use_mg = ctx->use_mg;
     WG_CUDA(cudaSetDevice(ctx->cfg.device));
     WG_CUDA(cudaIpcGetMemHandle(&b.handle, ctx->arena));
     std::memcpy(blob, &b, sizeof(b));
@@ -2998,10 +3555,11 @@ int wg_ctx_import_peer(wg_ctx* ctx, int gpu_index, const void* blob, size_t len)
     const int di = ctx->cfg.dtype == WG_F32 ? 0 : 1;
     if (b.use_nvl != ctx->use_nvl || b.use_split != ctx->use_split || b.split_span != ctx->split_span ||
         b.fence_scope != ctx->fence_scope || b.sms != ctx->sms || b.occ_split != ctx->occ_split[di] ||
-        b.occ_nvl != ctx->occ_nvl[di] || b.split_min_bytes != ctx->split_min_bytes || b.use_hier != ctx->use_hier)
+        b.occ_nvl != ctx->occ_nvl[di] || b.split_min_bytes != ctx->split_min_bytes || b.use_hier != ctx->use_hier ||
+        b.use_mg != ctx->use_mg)
         return fail(WG_EINVAL,
                     "peer %d runs different kernel settings (WG_NVL/WG_SPLIT/WG_SPLIT_SPAN/WG_SPLIT_MIN_BYTES/"
-                    "WG_FENCE_SCOPE/WG_HIER or SM count / occupancy differ)", gpu_index);
+                    "WG_FENCE_SCOPE/WG_HIER/WG_MG or SM count / occupancy differ)", gpu_index);
     if (gpu_index == ctx->cfg.gpu_index) return WG_OK;
     if (ctx->opened[gpu_index]) return WG_OK;
     WG_CUDA(cudaSetDevice(ctx->cfg.device));
@@ -3090,6 +3648,7 @@ static int occupancy(wg_ctx* ctx, int n_stage) {
 // Input-ring stages of wagma_local_kernel for a launch of n_jobs jobs (the W'
 // stage takes one chunk row per job); < 2 means the launch does not fit.
 static bool L_has_parts(const wg_ctx* ctx) { return ctx->L.part_ring > ctx->L.part_flags; }
+static bool L_has_red(const wg_ctx* ctx) { return ctx->L.red_ring > ctx->L.red_flags; }
 
 static int local_stages(wg_ctx* ctx, int n_jobs) {
     const int64_t row = int64_t(kLocChunkVecs) * 16;
@@ -3368,7 +3927,38 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         wide = wide || (__builtin_popcount(gpus) >= ctx->split_span && p.owners[k].n == p.plans[k].n_leaves &&
                         split_pays(p.owners[k].n, __builtin_popcount(gpus)));
     }
-    if (p.need_fence && !any_hier && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= ctx->split_span && wide &&
+    int mg_rows_in = 0, mg_cap_a = 0, mg_cap_b = 0;
+    if (any_hier && ctx->use_mg) {
+        // wagma_mg_kernel: input ring + W' stage + phase-1 rows (at least one
+        // chunk of every plan's leaves: the pull fallback) + phase-2 rows
+        const int64_t row = int64_t(kLocChunkVecs) * 16;
+        const int total_rows = int(ctx->mg_dyn_max[c.dtype == WG_F32 ? 0 : 1] / row);
+        mg_rows_in = WG_MG_IN_STAGES * 3 + n_jobs;
+        int n_split = 0;
+        for (int k = 0; k < p.n_plans; ++k) {
+            if (!p.plan_hl[k]) continue;
+            const int np = p.plans[k].n_leaves >> p.plan_hl[k];
+            unsigned gpus = 0;
+            for (int li = 0; li < p.plans[k].n_leaves; ++li) gpus |= 1u << (p.plans[k].leaves[li] / ctx->R);
+            n_split += ctx->use_split && L_has_red(ctx) && split_pays(np, __builtin_popcount(gpus));
+        }
+        mg_cap_b = std::min(4 * n_split, std::max(0, (total_rows - mg_rows_in) / 3));
+        mg_cap_a = total_rows - mg_rows_in - mg_cap_b;
+        if (mg_cap_a < n_leaves_total || (n_split && mg_cap_b < n_split)) mg_cap_a = 0;  // does not fit
+    }
+    if (mg_cap_a > 0) {
+        p.loc_stages = WG_MG_IN_STAGES;
+        p.mg_cap_a = mg_cap_a;
+        p.mg_cap_b = mg_cap_b;
+        p.mg_split = ctx->use_split && L_has_red(ctx);
+        const size_t smem_mg = size_t(mg_rows_in + mg_cap_a + mg_cap_b) * size_t(kLocChunkVecs) * 16;
+        const int64_t n_chunks = (ctx->n_tiles + kLocTiles - 1) / kLocTiles;
+        const int64_t g = std::min<int64_t>(n_chunks, ctx->sms);
+        if (c.dtype == WG_F32)
+            wagma_mg_kernel<float><<<unsigned(g), kMgThreads, smem_mg, s>>>(p);
+        else
+            wagma_mg_kernel<double><<<unsigned(g), kMgThreads, smem_mg, s>>>(p);
+    } else if (p.need_fence && !any_hier && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= ctx->split_span && wide &&
         c.n * int64_t(ctx->esize) >= ctx->split_min_bytes) {
         // split sums: every GPU of a job makes this same choice (it depends on
         // P and the process-wide knob only), so owners always publish the

@@ -39,10 +39,13 @@ def _run(tmp_path, G, port, env_extra=None, **kw):
     return [dict(np.load(os.path.join(tmp_path, f"rank{r}.npz"))) for r in range(G)]
 
 
-@pytest.fixture(params=["hier", "nohier"])
+@pytest.fixture(params=["mg", "nvl-hier", "nohier"])
 def hier(request):
-    """Hierarchical subtree-partial sums on (default) or off (split / pull kernels)."""
-    return {"WG_HIER": "1" if request.param == "hier" else "0"}
+    """Kernel family: hierarchical sums in the TMA-produce kernel (default),
+    hierarchical sums in the pull kernel (WG_MG=0), or no hierarchy (split /
+    pull kernels, WG_HIER=0)."""
+    return {"mg": {"WG_HIER": "1", "WG_MG": "1"}, "nvl-hier": {"WG_HIER": "1", "WG_MG": "0"},
+            "nohier": {"WG_HIER": "0", "WG_MG": "1"}}[request.param]
 
 
 CASES = [
@@ -61,7 +64,7 @@ CASES = [
 def test_multigpu_live_protocol_bit_exact(tmp_path, hier, G, P, S, T, tau, n, dtype, victims, alpha):
     if _ngpus() < G:
         pytest.skip(f"needs {G} GPUs")
-    port = 29400 + (hash((G, P, S, T, n, hier["WG_HIER"])) % 500)
+    port = 29400 + (hash((G, P, S, T, n, hier["WG_HIER"], hier["WG_MG"])) % 500)
     outs = _run(tmp_path, G, port, env_extra=hier, P=P, S=S, T=T, tau=tau, nelem=n, dtype=dtype, victims=victims,
                 alpha=alpha)
     R = P // G
@@ -136,7 +139,7 @@ def test_multigpu_baseline_size_bit_exact(tmp_path, hier, G, S):
 
     from paper_2005_00124_b200.driver import synthetic_grad
     P, T, tau, n = 8, 12, 10, 25_559_081
-    port = 29950 + (hash((G, S, hier["WG_HIER"])) % 40)
+    port = 29950 + (hash((G, S, hier["WG_HIER"], hier["WG_MG"])) % 40)
     env = dict(hier, WG_SPLIT_MIN_BYTES=str(8 << 20))
     outs = _run(tmp_path, G, port, env_extra=env, P=P, S=S, T=T, tau=tau, nelem=n, dtype="f32", victims=1,
                 pipelined=1, save_grads=0, delay_us=300)
