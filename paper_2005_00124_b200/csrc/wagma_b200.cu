@@ -1593,7 +1593,8 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
 #define WG_MG_IN_STAGES 3
 #endif
 constexpr int kMgLag1 = WG_MG_LAG1, kMgLag2 = WG_MG_LAG2;
-constexpr int kMgThreads = kLocConsumers + 96;  // + input producer, control/phase-1 puller, phase-2 puller
+constexpr int kMgThreads = kLocConsumers + 128;  // + input producer, control/phase-1 puller, phase-2 puller, publisher
+constexpr int kMgPub = 8;                         // chunks in flight between the consumers and the publisher
 constexpr int kMgMaxEff = 16;                   // effective leaves per plan
 enum MgMode : int8_t { kMgPull = 0, kMgHier = 1, kMgSplit = 2 };
 
@@ -1609,6 +1610,8 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
     __shared__ __align__(8) uint64_t fb[kMgMaxStagesB], eb[kMgMaxStagesB];       // phase-2 rows
     __shared__ volatile int ready;
     __shared__ int s_nsa, s_nsb, s_rows_a, s_rows_b;
+    // consumers -> publisher: chunk produced (pd) / owned chunk reduced (rd); acks (pk, rk)
+    __shared__ __align__(8) uint64_t pd[kMgPub], pk[kMgPub], rd[kMgPub], rk[kMgPub];
     // local partials: buffers, flags and their leaf jobs in leaf order
     __shared__ T* s_part[kMaxJobs];
     __shared__ int64_t* s_pflag[kMaxJobs];
@@ -1648,6 +1651,12 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
         for (int st = 0; st < kMgMaxStagesB; ++st) {
             mbar_init(&fb[st], 1);
             mbar_init(&eb[st], kLocConsumers / 32);
+        }
+        for (int k = 0; k < kMgPub; ++k) {
+            mbar_init(&pd[k], kLocConsumers / 32);
+            mbar_init(&rd[k], kLocConsumers / 32);
+            mbar_init(&pk[k], 1);
+            mbar_init(&rk[k], 1);
         }
         for (int k = 0; k < J; ++k) {  // the producers' job order -> partial leaf lists
             const int pid = p.job_part[k];
@@ -1912,23 +1921,73 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 ++k;
             }
         }
-    } else {
-        // ---------------- consumers ----------------
-        const int ct = tid - 96;
-        const int cw = ct >> 5;
-        unsigned bad = 0;
-        int sti = 0, sta = 0, stb = 0;
-        unsigned phi = 0, pha = 0, phb = 0;
-        int64_t ka = 0, kb = 0;
-        bool ok = true, resolved = false;
-        // consumers-only named barrier (id 1)
-        auto cbar = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(kLocConsumers) : "memory"); };
+    } else if (warp == 3) {
+        // ---------------- publisher: fences and readiness flags ----------------
+        // Walks the consumers' sequence (produce i, then phase 1 of i - lag):
+        // waits for every consumer warp's arrival, issues one fence
+        // (cumulative over their stores, acquired through the mbarrier) and
+        // raises the flags, so no consumer ever waits on a fence.
         auto fence_pub = [&]() {
             if (p.fence_scope == 0)
                 fence_sys();
             else if (p.fence_scope == 1)
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
         };
+        int64_t nown = 0;
+        bool res = true;
+        for (int64_t i = 0; res && i < my_nchunks + kMgLag1; ++i) {
+            if (i < my_nchunks) {
+                const int slot = int(i % kMgPub);
+                if (!mbar_wait(p, &pd[slot], unsigned((i / kMgPub) & 1))) break;
+                if (lane == 0) fence_pub();
+                __syncwarp();
+                const int64_t c = int64_t(blockIdx.x) + i * gridDim.x;
+                const int64_t t0 = c * kLocTiles;
+                const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
+                for (int e = lane; e < J * nt * kWarps; e += 32) {
+                    const int w = e % kWarps, tt = (e / kWarps) % nt, j = e / (kWarps * nt);
+                    const DevJob& jb = p.jobs[j];
+                    if (jb.produces) st_relaxed_sys(flag_ptr(p, jb.rank, t0 + tt, w), jb.version);
+                }
+                for (int e = lane; e < p.n_parts * nt; e += 32)
+                    st_relaxed_sys(s_pflag[e / nt] + t0 + e % nt, p.part_version[e / nt]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pk[slot]);
+            }
+            const int64_t x1 = i - kMgLag1;
+            if (x1 < 0 || x1 >= my_nchunks) continue;
+            if (x1 == 0) {
+                while (ready == 0) __nanosleep(64);
+                __threadfence_block();
+                res = ready == 1;
+                if (!res) break;
+            }
+            bool owned = false;
+            for (int pl = 0; pl < NP; ++pl) owned = owned || (s_mode[pl] == kMgSplit && s_ownlocal[pl][owner(pl, x1)]);
+            if (!owned) continue;
+            const int slot = int(nown % kMgPub);
+            if (!mbar_wait(p, &rd[slot], unsigned((nown / kMgPub) & 1))) break;
+            if (lane == 0) fence_pub();
+            __syncwarp();
+            const int64_t c = int64_t(blockIdx.x) + x1 * gridDim.x;
+            const int64_t t0 = c * kLocTiles;
+            const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
+            for (int pl = 0; pl < NP; ++pl)
+                if (s_mode[pl] == kMgSplit && s_ownlocal[pl][owner(pl, x1)] && lane < nt)
+                    st_relaxed_sys(s_redflag[pl][owner(pl, x1)] + t0 + lane, s_ver[pl]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rk[slot]);
+            ++nown;
+        }
+    } else {
+        // ---------------- consumers ----------------
+        const int ct = tid - 128;
+        const int cw = ct >> 5;
+        unsigned bad = 0;
+        int sti = 0, sta = 0, stb = 0;
+        unsigned phi = 0, pha = 0, phb = 0;
+        int64_t nown = 0;  // owned reduced chunks handed to the publisher
+        bool ok = true, resolved = false;
         for (int64_t i = 0; ok && i < my_nchunks + kMgLag2; ++i) {
             if (i < my_nchunks) {
                 // ---- produce chunk i ----
@@ -1962,20 +2021,15 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                         __stcg(reinterpret_cast<V*>(s_part[pid] + idx), tree_sum<T>(fetch, s_plog[pid]));
                     }
                 }
-                // publish: every consumer's stores, one fence, the chunk's flags
-                cbar();
-                if (cw == 0) {
-                    if (lane == 0) fence_pub();
-                    __syncwarp();
-                    const int64_t t0 = c * kLocTiles;
-                    const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
-                    for (int e = lane; e < J * nt * kWarps; e += 32) {
-                        const int w = e % kWarps, tt = (e / kWarps) % nt, j = e / (kWarps * nt);
-                        const DevJob& jb = p.jobs[j];
-                        if (jb.produces) st_relaxed_sys(flag_ptr(p, jb.rank, t0 + tt, w), jb.version);
+                // hand the chunk to the publisher (fence + flags off this path)
+                {
+                    const int slot = int(i % kMgPub);
+                    if (i >= kMgPub && !mbar_wait(p, &pk[slot], unsigned(((i / kMgPub) - 1) & 1))) {
+                        ok = false;
+                        break;
                     }
-                    for (int e = lane; e < p.n_parts * nt; e += 32)
-                        st_relaxed_sys(s_pflag[e / nt] + t0 + e % nt, p.part_version[e / nt]);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&pd[slot]);
                 }
             }
             if (!resolved && i >= kMgLag1) {
@@ -2021,18 +2075,15 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&ea[sta]);
                     if (++sta == s_nsa) sta = 0, pha ^= 1u;
-                    ++ka;
-                    if (owned) {
-                        cbar();
-                        if (cw == 0) {
-                            if (lane == 0) fence_pub();
-                            __syncwarp();
-                            const int64_t t0 = c * kLocTiles;
-                            const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
-                            for (int pl = 0; pl < NP; ++pl)
-                                if (s_mode[pl] == kMgSplit && s_ownlocal[pl][owner(pl, x1)] && lane < nt)
-                                    st_relaxed_sys(s_redflag[pl][owner(pl, x1)] + t0 + lane, s_ver[pl]);
+                    if (owned) {  // the reduced chunk to the publisher
+                        const int slot = int(nown % kMgPub);
+                        if (nown >= kMgPub && !mbar_wait(p, &rk[slot], unsigned(((nown / kMgPub) - 1) & 1))) {
+                            ok = false;
+                            break;
                         }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&rd[slot]);
+                        ++nown;
                     }
                 }
             }
@@ -2067,7 +2118,6 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&eb[stb]);
                     if (++stb == s_nsb) stb = 0, phb ^= 1u;
-                    ++kb;
                 }
             }
         }

@@ -27,7 +27,7 @@ __all__ = ["ReplicaDiagnostics", "replica_diagnostics", "gamma_bound", "check_af
 class ReplicaDiagnostics:
     mu: torch.Tensor          # fp64 replica mean over all P ranks
     gamma: float              # sum_r ||W_r - mu||^2 over all P ranks
-    identical: bool           # every replica bit-identical (gamma == 0 exactly)
+    identical: bool           # every replica bit-identical (the reference's np.array_equal check)
 
 
 def replica_diagnostics(ctx: DeviceContext, replicas: Mapping[int, torch.Tensor],
@@ -49,10 +49,23 @@ def replica_diagnostics(ctx: DeviceContext, replicas: Mapping[int, torch.Tensor]
     out = torch.zeros(2, dtype=torch.float64, device=ctx.torch_device)
     ctx._raise(ctx.lib.wg_replicas_spread(ctx._h, ptrs, len(ranks), mu.data_ptr(), out.data_ptr(), stream),
                "wg_replicas_spread")
+    # bit identity (optim.py:289-291): out[1] = max |W_r - W_first| over the
+    # local replicas (exact); across GPUs the first local replicas must also
+    # agree bit for bit -- compared through two integer checksums of their bits
+    first = replicas[ranks[0]]
+    bits = first.view(torch.int32 if first.dtype == torch.float32 else torch.int64).to(torch.int64)
+    ident = torch.stack([out[1], (bits.sum() & 0xFFFFFFFFFFFF).to(torch.float64),
+                         (((bits * 0x9E3779B1) % 1000000007).sum() & 0xFFFFFFFFFFFF).to(torch.float64)])
     if multi:
         dist.all_reduce(out[:1], group=process_group)
+        lo, hi = ident.clone(), ident.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=process_group)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=process_group)
+        identical = bool(hi[0].item() == 0.0 and torch.equal(lo[1:], hi[1:]))
+    else:
+        identical = bool(ident[0].item() == 0.0)
     gamma = float(out[0].item())
-    return ReplicaDiagnostics(mu=mu, gamma=gamma, identical=gamma == 0.0)
+    return ReplicaDiagnostics(mu=mu, gamma=gamma, identical=identical)
 
 
 def gamma_bound(P: int, eta: float, M_hat: float, tau: int) -> float:
