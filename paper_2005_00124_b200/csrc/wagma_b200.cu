@@ -1260,6 +1260,9 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 #ifndef WG_LOC_RING_CS  // send-ring stores evict-first (.cs) instead of .cg
 #define WG_LOC_RING_CS 1
 #endif
+#ifndef WG_LOC_STACK  // 1: plans summed in registers in leaf order (no W' stage), shared memory all input ring
+#define WG_LOC_STACK 1
+#endif
 constexpr int kLocTiles = WG_LOC_TILES;                    // tiles per chunk (per item)
 constexpr int kLocConsumers = WG_LOC_CONSUMER_WARPS * 32;  // consumer threads
 constexpr int kLocThreads = kLocConsumers + 64;            // + producer warp + control warp
@@ -1286,7 +1289,8 @@ struct LocJob {
 // stores, W' into the thread-private stage. FULL: the chunk lies inside n.
 template <typename T, bool FULL>
 __device__ __forceinline__ unsigned loc_item(const LaunchParams& p, const LocJob<T>& jb, int j, int64_t e0,
-                                             const typename Tr<T>::V* r, typename Tr<T>::V* wst, int ct) {
+                                             const typename Tr<T>::V* r, typename Tr<T>::V* wst, int ct,
+                                             typename Tr<T>::V* out = nullptr) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
     unsigned bad = 0;
@@ -1324,9 +1328,41 @@ __device__ __forceinline__ unsigned loc_item(const LaunchParams& p, const LocJob
             else
                 __stcg(reinterpret_cast<V*>(jb.ring + idx), wp);
         }
-        wst[j * kLocChunkVecs + v] = wp;
+        if (wst) wst[j * kLocChunkVecs + v] = wp;
+        if (out) out[kv] = wp;
     }
     return bad << j;
+}
+
+// Butterfly register stack: push leaf `pos` (its bits say which finished
+// subtrees it closes); returns the combined value (the plan's sum at its
+// last leaf). Same pairing as TreeSum (collective.py:310-329).
+template <typename V, int U>
+__device__ __forceinline__ void stack_push(V (&s)[5][U], V (&v)[U], int pos) {
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+        if (pos & 1) {
+            v[k] = vadd(s[0][k], v[k]);
+            if (pos & 2) {
+                v[k] = vadd(s[1][k], v[k]);
+                if (pos & 4) {
+                    v[k] = vadd(s[2][k], v[k]);
+                    if (pos & 8) {
+                        v[k] = vadd(s[3][k], v[k]);
+                        s[4][k] = v[k];
+                    } else {
+                        s[3][k] = v[k];
+                    }
+                } else {
+                    s[2][k] = v[k];
+                }
+            } else {
+                s[1][k] = v[k];
+            }
+        } else {
+            s[0][k] = v[k];
+        }
+    }
 }
 
 template <typename T>
@@ -1350,7 +1386,7 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
     const int64_t chunk_elems = int64_t(kLocChunkVecs) * E;
     const int64_t n_chunks = (p.n_tiles + kLocTiles - 1) / kLocTiles;
     V* rows = reinterpret_cast<V*>(dyn_smem);               // [NS][3][kLocChunkVecs]: W, g, m of an item
-    V* wst = rows + size_t(NS) * 3 * kLocChunkVecs;         // [J][kLocChunkVecs]: W' of every job
+    V* wst = WG_LOC_STACK ? nullptr : rows + size_t(NS) * 3 * kLocChunkVecs;  // [J][kLocChunkVecs]: W' of every job
     if (tid == 0) {
         sm.abort = 0;
         ready = 0;
@@ -1397,7 +1433,8 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
                 // TMA, the ragged end is read by the consumers from global memory
                 const int64_t rem = (p.n - e0) * int64_t(sizeof(T));
                 const unsigned bytes = rem >= chunk_bytes ? chunk_bytes : (rem > 0 ? unsigned(rem) & ~15u : 0u);
-                for (int j = 0; j < J; ++j, ++k) {
+                for (int jj = 0; jj < J; ++jj, ++k) {
+                    const int j = WG_LOC_STACK ? p.job_order[jj] : jj;
                     if (k >= NS && !mbar_wait(p, &empty[st], ph ^ 1u)) {
                         ok = false;
                         break;
@@ -1459,7 +1496,7 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
                     s_memW[pl][mi] = static_cast<T*>(jb.W);
                 }
                 s_nmem[pl] = int8_t(P_.n_members);
-                s_fast[pl] = fast && P_.divisor_pow2;
+                s_fast[pl] = fast && P_.divisor_pow2 && (!WG_LOC_STACK || p.plan_hl[pl]);
             }
         }
         res = __shfl_sync(0xffffffffu, res, 0);
@@ -1477,6 +1514,80 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
         for (int64_t c = blockIdx.x; c < n_chunks && ok; c += gridDim.x) {
             const int64_t e0 = c * chunk_elems;
             const bool fullc = e0 + chunk_elems <= p.n;
+#if WG_LOC_STACK
+            // jobs in the host's leaf order: each plan's sum builds up in a
+            // register stack and is finished at its last leaf
+            V stk[5][kLocVPT];
+            for (int jj = 0; jj < J; ++jj) {
+                const int j = p.job_order[jj];
+                if (!mbar_wait(p, &full[st], ph)) {
+                    ok = false;
+                    break;
+                }
+                const V* r = rows + size_t(st) * 3 * kLocChunkVecs;
+                V wp[kLocVPT];
+                if (fullc)
+                    bad |= loc_item<T, true>(p, s_job[j], j, e0, r, nullptr, ct, wp);
+                else
+                    bad |= loc_item<T, false>(p, s_job[j], j, e0, r, nullptr, ct, wp);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+                if (++st == NS) st = 0, ph ^= 1u;
+                const int pl = p.job_part[jj];
+                if (pl < 0) continue;
+                stack_push<V, kLocVPT>(stk, wp, p.job_ppos[jj]);
+                if (!p.job_plast[jj]) continue;
+                if (!resolved) {
+                    while (ready == 0) __nanosleep(32);
+                    __threadfence_block();
+                    if (ready != 1) {
+                        ok = false;
+                        break;
+                    }
+                    resolved = true;
+                }
+                if (fullc && s_fast[pl]) {
+                    // every member timely: one average, stored to each replica
+                    const T inv = T(1) / T(p.plans[pl].divisor);
+                    const int nm = s_nmem[pl];
+#pragma unroll
+                    for (int kv = 0; kv < kLocVPT; ++kv) {
+                        const int64_t idx = e0 + int64_t(kv * kLocConsumers + ct) * E;
+                        const V avg = vscale(inv, wp[kv]);
+                        for (int mi = 0; mi < nm; ++mi) __stcs(reinterpret_cast<V*>(s_memW[pl][mi] + idx), avg);
+                    }
+                }
+            }
+            if (!ok) break;
+            if (!resolved) {
+                while (ready == 0) __nanosleep(32);
+                __threadfence_block();
+                if (ready != 1) break;
+                resolved = true;
+            }
+            // plans not finished from the stack: the generic sum, W' read
+            // back from the send slots this thread wrote
+            for (int pl = 0; pl < p.n_plans; ++pl) {
+                if (fullc && s_fast[pl]) continue;
+                const DevPlan& P_ = p.plans[pl];
+#pragma unroll
+                for (int kv = 0; kv < kLocVPT; ++kv) {
+                    const int v = kv * kLocConsumers + ct;
+                    const int64_t idx = e0 + int64_t(v) * E;
+                    if (idx >= p.npad) continue;
+                    auto fetch = [&](int leaf) -> V {
+                        const int src = sm.leaf_src[pl][leaf];
+                        if (src >= 0) return __ldcg(reinterpret_cast<const V*>(s_job[src].ring + idx));
+                        return __ldcg(reinterpret_cast<const V*>(
+                            ring_ptr<T>(p, P_.leaves[leaf], sm.leaf_slot[pl][leaf]) + idx));
+                    };
+                    finish_members<T>(p, sm, P_, tree_sum<T>(fetch, P_.log_leaves), idx, [&](int j) {
+                        return __ldcg(reinterpret_cast<const V*>(s_job[j].ring + idx));
+                    });
+                }
+            }
+            continue;
+#endif
             for (int j = 0; j < J; ++j) {
                 if (!mbar_wait(p, &full[st], ph)) {
                     ok = false;
@@ -1629,6 +1740,11 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
     __shared__ int64_t s_ver[kMaxPlans];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int J = p.n_jobs, NSI = p.loc_stages, NP = p.n_plans;
+    // optional per-CTA cycle counters (tools/phase_profile.py, WG_PROF_MG=1): 16 slots
+    const long long kt0 = clock64();
+    auto prof_add = [&](int slot, long long v) {
+        if (p.prof) p.prof[blockIdx.x * 16 + slot] += v;
+    };
     constexpr int C = kLocChunkVecs;
     const int64_t chunk_elems = int64_t(C) * E;
     const int64_t n_chunks = (p.n_tiles + kLocTiles - 1) / kLocTiles;
@@ -1753,10 +1869,12 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 const unsigned bytes = rem >= chunk_bytes_full ? chunk_bytes_full : (rem > 0 ? unsigned(rem) & ~15u : 0u);
                 for (int jj = 0; jj < J; ++jj, ++k) {
                     const int j = p.job_order[jj];
+                    const long long w0 = p.prof ? clock64() : 0;
                     if (k >= NSI && !mbar_wait(p, &ein[st], ph ^ 1u)) {
                         ok = false;
                         break;
                     }
+                    if (p.prof) prof_add(12, clock64() - w0);
                     const LocJob<T>& jb = s_job[j];
                     V* dst = rows_in + size_t(st) * 3 * C;
                     if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
@@ -1777,6 +1895,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 raise_error(p, WG_ETIMEOUT, k);
                 sm.abort = 1;
             }
+            prof_add(13, clock64() - kt0);
         }
     } else if (warp == 1) {
         // ---------------- control + phase-1 puller ----------------
@@ -1839,6 +1958,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
         if (lane == 0) {
             __threadfence_block();
             ready = res ? 1 : 2;
+            prof_add(11, clock64() - kt0);
         }
         __syncwarp();
         const int NSA = s_nsa;
@@ -1850,16 +1970,23 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
             rows_of(kc, ra, rb);
             if (!ra) continue;
             const int64_t c = int64_t(blockIdx.x) + kc * gridDim.x;
+            const long long w0 = clock64();
             if (k >= NSA && !mbar_wait(p, &ea[st], ph ^ 1u)) {
                 if (lane == 0) raise_error(p, WG_ETIMEOUT, kc);
                 break;
             }
+            const long long w1 = clock64();
             // wait for every source of the chunk (lane e polls source e), then copy
             int rc = 0, e = 0;
             for (int pl = 0; pl < NP; ++pl) {
                 if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, kc)]) continue;
                 for (int u = 0; u < s_ne[pl]; ++u, ++e)
                     if ((e & 31) == lane && !rc) rc = poll(s_eflag[pl][u], s_estride[pl][u], s_ewant[pl][u], c);
+            }
+            __syncwarp();
+            if (lane == 0 && p.prof) {
+                prof_add(6, w1 - w0);
+                prof_add(5, clock64() - w1);
             }
             if (rc) raise_error(p, rc, kc);
             if (__any_sync(0xffffffffu, rc != 0)) break;
@@ -1878,6 +2005,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
             if (++st == NSA) st = 0, ph ^= 1u;
             ++k;
         }
+        if (lane == 0) prof_add(7, clock64() - kt0);
     } else if (warp == 2) {
         // ---------------- phase-2 puller: owners' reduced chunks ----------------
         while (ready == 0) __nanosleep(64);
@@ -1938,9 +2066,15 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
         for (int64_t i = 0; res && i < my_nchunks + kMgLag1; ++i) {
             if (i < my_nchunks) {
                 const int slot = int(i % kMgPub);
+                const long long w0 = clock64();
                 if (!mbar_wait(p, &pd[slot], unsigned((i / kMgPub) & 1))) break;
+                const long long w1 = clock64();
                 if (lane == 0) fence_pub();
                 __syncwarp();
+                if (lane == 0 && p.prof) {
+                    prof_add(8, w1 - w0);
+                    prof_add(9, clock64() - w1);
+                }
                 const int64_t c = int64_t(blockIdx.x) + i * gridDim.x;
                 const int64_t t0 = c * kLocTiles;
                 const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
@@ -1979,6 +2113,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
             if (lane == 0) mbar_arrive(&rk[slot]);
             ++nown;
         }
+        if (lane == 0) prof_add(10, clock64() - kt0);
     } else {
         // ---------------- consumers ----------------
         const int ct = tid - 128;
@@ -1996,10 +2131,12 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 const bool fullc = e0 + chunk_elems <= p.n;
                 for (int jj = 0; jj < J; ++jj) {
                     const int j = p.job_order[jj];
+                    const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
                     if (!mbar_wait(p, &fin[sti], phi)) {
                         ok = false;
                         break;
                     }
+                    if (p.prof && ct == 0) prof_add(1, clock64() - w0);
                     const V* r = rows_in + size_t(sti) * 3 * C;
                     if (fullc)
                         bad |= loc_item<T, true>(p, s_job[j], j, e0, r, wst, ct);
@@ -2024,16 +2161,20 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 // hand the chunk to the publisher (fence + flags off this path)
                 {
                     const int slot = int(i % kMgPub);
+                    const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
                     if (i >= kMgPub && !mbar_wait(p, &pk[slot], unsigned(((i / kMgPub) - 1) & 1))) {
                         ok = false;
                         break;
                     }
+                    if (p.prof && ct == 0) prof_add(3, clock64() - w0);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&pd[slot]);
                 }
             }
             if (!resolved && i >= kMgLag1) {
+                const long long w0 = clock64();
                 while (ready == 0) __nanosleep(32);
+                if (p.prof && ct == 0) prof_add(4, clock64() - w0);
                 __threadfence_block();
                 if (ready != 1) break;
                 resolved = true;
@@ -2046,10 +2187,12 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 int ra, rb;
                 rows_of(x1, ra, rb);
                 if (ra) {
+                    const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
                     if (!mbar_wait(p, &fa[sta], pha)) {
                         ok = false;
                         break;
                     }
+                    if (p.prof && ct == 0) prof_add(2, clock64() - w0);
                     const V* lb = rows_a + size_t(sta) * s_rows_a * C;
                     bool owned = false;
                     int e = 0;
@@ -2126,6 +2269,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
             sm.abort = 1;
         }
         report_divergence(p, bad);
+        if (ct == 0) prof_add(0, clock64() - kt0);
     }
     unsigned my_tiles = 0;
     for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x)
@@ -3702,7 +3846,7 @@ static bool L_has_red(const wg_ctx* ctx) { return ctx->L.red_ring > ctx->L.red_f
 
 static int local_stages(wg_ctx* ctx, int n_jobs) {
     const int64_t row = int64_t(kLocChunkVecs) * 16;
-    const int64_t avail = int64_t(ctx->loc_dyn_max[ctx->cfg.dtype == WG_F32 ? 0 : 1]) - int64_t(n_jobs) * row;
+    const int64_t avail = int64_t(ctx->loc_dyn_max[ctx->cfg.dtype == WG_F32 ? 0 : 1]) - (WG_LOC_STACK ? 0 : int64_t(n_jobs) * row);
     if (avail < 2 * 3 * row) return 0;
     return int(std::min<int64_t>(kLocMaxStages, avail / (3 * row)));
 }
@@ -3887,6 +4031,38 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
     for (int j = 0; j < n_jobs; ++j) {
         p.job_order[j] = int8_t(j);
         p.job_part[j] = -1;
+    }
+    // Single GPU (register-stack kernel): jobs in each plan's leaf order when
+    // every leaf is a distinct job of this launch at the plan's version
+    // (plan_hl = 1 marks such a plan; the device confirms with the stamps)
+    if (!p.need_fence && WG_LOC_STACK) {
+        int nord = 0;
+        bool placed[kMaxJobs] = {};
+        for (int k = 0; k < p.n_plans; ++k) {
+            const DevPlan& P_ = p.plans[k];
+            bool ok = P_.n_leaves <= 16 && p.owners[k].n == P_.n_leaves;
+            for (int li = 0; li < P_.n_leaves && ok; ++li) {
+                const int jq = p.job_of_rank[P_.leaves[li]];
+                ok = jq >= 0 && p.jobs[jq].produces && p.jobs[jq].vidx == P_.vidx && !placed[jq];
+            }
+            p.plan_hl[k] = int8_t(ok);
+            if (!ok) continue;
+            for (int li = 0; li < P_.n_leaves; ++li) {
+                const int jq = p.job_of_rank[P_.leaves[li]];
+                placed[jq] = true;
+                p.job_order[nord] = int8_t(jq);
+                p.job_part[nord] = int8_t(k);
+                p.job_ppos[nord] = int8_t(li);
+                p.job_plast[nord] = int8_t(li == P_.n_leaves - 1);
+                ++nord;
+            }
+        }
+        for (int j = 0; j < n_jobs; ++j)
+            if (!placed[j]) {
+                p.job_order[nord] = int8_t(j);
+                p.job_part[nord] = -1;
+                ++nord;
+            }
     }
     // Hierarchical sums: a plan spanning GPUs whose lowest hl tree levels
     // stay inside one GPU (masks < R under the block rank mapping,
@@ -4080,7 +4256,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
     } else if (!p.need_fence && ctx->use_loc &&
                (p.loc_stages = local_stages(ctx, n_jobs)) >= 2) {
         const size_t row = size_t(kLocChunkVecs) * 16;
-        const size_t loc_smem = (size_t(p.loc_stages) * 3 + size_t(n_jobs)) * row;
+        const size_t loc_smem = (size_t(p.loc_stages) * 3 + (WG_LOC_STACK ? 0 : size_t(n_jobs))) * row;
         const int64_t n_chunks = (ctx->n_tiles + kLocTiles - 1) / kLocTiles;
         const int64_t g = std::min<int64_t>(n_chunks, ctx->sms);
         if (c.dtype == WG_F32)

@@ -34,7 +34,8 @@ ctx = DeviceContext(a.P, a.S, a.nelem, tau=a.tau, n_gpus=G, gpu_index=rank, devi
 opt = GroupAveragingOptimizer(ctx, OptimizerConfig(T=1 << 30, S=a.S, tau=a.tau, eta=EtaSchedule(value=0.1),
                                                    update_rule="momentum"), torch.zeros(a.nelem, device=dev))
 g = {r: torch.randn(a.nelem, device=dev) * 0.01 for r in ctx.local_ranks}
-prof = torch.zeros(ctx.grid * 16, dtype=torch.int64, device=dev)
+prof = torch.zeros(max(ctx.grid, ctx.lib_sms if hasattr(ctx, "lib_sms") else 148) * 16, dtype=torch.int64,
+                   device=dev)
 ctx.lib.wg_ctx_set_profile(ctx._h, ctypes.c_void_p(prof.data_ptr()))
 ghz = 1.965
 for t in range(a.iters):
@@ -50,9 +51,13 @@ for t in range(a.iters):
     torch.cuda.synchronize()
     t = t * 8 + 7
     if True:
-        split_prof = os.environ.get("WG_PROF_SPLIT", "0") == "1"
+        split_prof = os.environ.get("WG_PROF_SPLIT", "0") == "1" or os.environ.get("WG_PROF_MG", "0") == "1"
         p = prof.view(-1, 16 if split_prof else 8).cpu().numpy().astype(np.float64)
-        if os.environ.get("WG_PROF_SPLIT", "0") == "1":
+        if os.environ.get("WG_PROF_MG", "0") == "1":
+            names = ["cons_total", "cons_in_wait", "cons_ph1_wait", "cons_ack_wait", "cons_ready_wait",
+                     "pullA_poll", "pullA_empty", "pullA_total", "pub_wait", "pub_fence", "pub_total",
+                     "ready_at", "prod_empty_wait", "prod_total", "x", "x"]
+        elif os.environ.get("WG_PROF_SPLIT", "0") == "1":
             names = ["producer_total", "pullA_total", "x", "redA_full_wait", "redA_total", "pullB_total", "finB_full_wait", "finB_total", "pullA_empty", "pullA_poll", "x", "pullB_empty", "pullB_poll", "x", "fin_ready_at", "fin_work"]
         elif os.environ.get("WG_NVL", "1") != "0":
             names = ["producer_total", "pull_empty_wait", "pull_poll", "pull_issue", "cons_full_wait", "x", "cons_total", "cons_ready_wait"]
