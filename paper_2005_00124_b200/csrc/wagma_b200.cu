@@ -1261,7 +1261,7 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 #define WG_LOC_RING_CS 1
 #endif
 #ifndef WG_LOC_STACK  // 1: plans summed in registers in leaf order (no W' stage), shared memory all input ring
-#define WG_LOC_STACK 1
+#define WG_LOC_STACK 0
 #endif
 constexpr int kLocTiles = WG_LOC_TILES;                    // tiles per chunk (per item)
 constexpr int kLocConsumers = WG_LOC_CONSUMER_WARPS * 32;  // consumer threads
@@ -1703,7 +1703,11 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
 #ifndef WG_MG_IN_STAGES
 #define WG_MG_IN_STAGES 3
 #endif
+#ifndef WG_MG_PUB_BATCH
+#define WG_MG_PUB_BATCH 1
+#endif
 constexpr int kMgLag1 = WG_MG_LAG1, kMgLag2 = WG_MG_LAG2;
+constexpr int kMgPubBatch = WG_MG_PUB_BATCH;  // chunks published per fence (< kMgPub)
 constexpr int kMgThreads = kLocConsumers + 128;  // + input producer, control/phase-1 puller, phase-2 puller, publisher
 constexpr int kMgPub = 8;                         // chunks in flight between the consumers and the publisher
 constexpr int kMgMaxEff = 16;                   // effective leaves per plan
@@ -2068,25 +2072,32 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 const int slot = int(i % kMgPub);
                 const long long w0 = clock64();
                 if (!mbar_wait(p, &pd[slot], unsigned((i / kMgPub) & 1))) break;
-                const long long w1 = clock64();
-                if (lane == 0) fence_pub();
-                __syncwarp();
-                if (lane == 0 && p.prof) {
-                    prof_add(8, w1 - w0);
-                    prof_add(9, clock64() - w1);
+                // chunks are published in batches of kMgPubBatch: one fence per batch
+                if ((i + 1) % kMgPubBatch == 0 || i + 1 == my_nchunks) {
+                    const long long w1 = clock64();
+                    if (lane == 0) fence_pub();
+                    __syncwarp();
+                    if (lane == 0 && p.prof) {
+                        prof_add(8, w1 - w0);
+                        prof_add(9, clock64() - w1);
+                    }
+                    for (int64_t b = i - i % kMgPubBatch; b <= i; ++b) {
+                        const int64_t c = int64_t(blockIdx.x) + b * gridDim.x;
+                        const int64_t t0 = c * kLocTiles;
+                        const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
+                        for (int e = lane; e < J * nt * kWarps; e += 32) {
+                            const int w = e % kWarps, tt = (e / kWarps) % nt, j = e / (kWarps * nt);
+                            const DevJob& jb = p.jobs[j];
+                            if (jb.produces) st_relaxed_sys(flag_ptr(p, jb.rank, t0 + tt, w), jb.version);
+                        }
+                        for (int e = lane; e < p.n_parts * nt; e += 32)
+                            st_relaxed_sys(s_pflag[e / nt] + t0 + e % nt, p.part_version[e / nt]);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&pk[int(b % kMgPub)]);
+                    }
+                } else if (lane == 0 && p.prof) {
+                    prof_add(8, clock64() - w0);
                 }
-                const int64_t c = int64_t(blockIdx.x) + i * gridDim.x;
-                const int64_t t0 = c * kLocTiles;
-                const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
-                for (int e = lane; e < J * nt * kWarps; e += 32) {
-                    const int w = e % kWarps, tt = (e / kWarps) % nt, j = e / (kWarps * nt);
-                    const DevJob& jb = p.jobs[j];
-                    if (jb.produces) st_relaxed_sys(flag_ptr(p, jb.rank, t0 + tt, w), jb.version);
-                }
-                for (int e = lane; e < p.n_parts * nt; e += 32)
-                    st_relaxed_sys(s_pflag[e / nt] + t0 + e % nt, p.part_version[e / nt]);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&pk[slot]);
             }
             const int64_t x1 = i - kMgLag1;
             if (x1 < 0 || x1 >= my_nchunks) continue;
