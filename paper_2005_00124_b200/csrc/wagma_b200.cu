@@ -1287,17 +1287,18 @@ struct LocJob {
 
 // Consumer work for one item (job j of a chunk): local step, m and send-ring
 // stores, W' into the thread-private stage. FULL: the chunk lies inside n.
-template <typename T, bool FULL>
+template <typename T, bool FULL, int NT = kLocConsumers>
 __device__ __forceinline__ unsigned loc_item(const LaunchParams& p, const LocJob<T>& jb, int j, int64_t e0,
                                              const typename Tr<T>::V* r, typename Tr<T>::V* wst, int ct,
                                              typename Tr<T>::V* out = nullptr) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
+    constexpr int VPT = kLocChunkVecs / NT;
     unsigned bad = 0;
     const bool sum = jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM;
 #pragma unroll
-    for (int kv = 0; kv < kLocVPT; ++kv) {
-        const int v = kv * kLocConsumers + ct;
+    for (int kv = 0; kv < VPT; ++kv) {
+        const int v = kv * NT + ct;
         const int64_t idx = e0 + int64_t(v) * E;
         const bool tail = !FULL && idx + E > p.n;  // ragged end: global loads, zero-filled
         V wp;
@@ -1708,7 +1709,16 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
 #endif
 constexpr int kMgLag1 = WG_MG_LAG1, kMgLag2 = WG_MG_LAG2;
 constexpr int kMgPubBatch = WG_MG_PUB_BATCH;  // chunks published per fence (< kMgPub)
-constexpr int kMgThreads = kLocConsumers + 128;  // + input producer, control/phase-1 puller, phase-2 puller, publisher
+#ifndef WG_MG_PROD_WARPS
+#define WG_MG_PROD_WARPS 8
+#endif
+#ifndef WG_MG_FIN_WARPS
+#define WG_MG_FIN_WARPS 8
+#endif
+constexpr int kMgProd = WG_MG_PROD_WARPS * 32;  // producer threads (W', partials)
+constexpr int kMgFin = WG_MG_FIN_WARPS * 32;    // finisher threads (phase 1 and 2)
+// + input TMA warp, control/phase-1 puller, phase-2 puller, publisher
+constexpr int kMgThreads = 128 + kMgProd + kMgFin;
 constexpr int kMgPub = 8;                         // chunks in flight between the consumers and the publisher
 constexpr int kMgMaxEff = 16;                   // effective leaves per plan
 enum MgMode : int8_t { kMgPull = 0, kMgHier = 1, kMgSplit = 2 };
@@ -1762,19 +1772,19 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
         ready = 0;
         for (int st = 0; st < NSI; ++st) {
             mbar_init(&fin[st], 1);
-            mbar_init(&ein[st], kLocConsumers / 32);
+            mbar_init(&ein[st], kMgProd / 32);
         }
         for (int st = 0; st < kMgMaxStagesA; ++st) {
             mbar_init(&fa[st], 1);
-            mbar_init(&ea[st], kLocConsumers / 32);
+            mbar_init(&ea[st], kMgFin / 32);
         }
         for (int st = 0; st < kMgMaxStagesB; ++st) {
             mbar_init(&fb[st], 1);
-            mbar_init(&eb[st], kLocConsumers / 32);
+            mbar_init(&eb[st], kMgFin / 32);
         }
         for (int k = 0; k < kMgPub; ++k) {
-            mbar_init(&pd[k], kLocConsumers / 32);
-            mbar_init(&rd[k], kLocConsumers / 32);
+            mbar_init(&pd[k], kMgProd / 32);
+            mbar_init(&rd[k], kMgFin / 32);
             mbar_init(&pk[k], 1);
             mbar_init(&rk[k], 1);
         }
@@ -2125,73 +2135,84 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
             ++nown;
         }
         if (lane == 0) prof_add(10, clock64() - kt0);
-    } else {
-        // ---------------- consumers ----------------
+    } else if (warp < 4 + kMgProd / 32) {
+        // ---------------- producers: W', partials ----------------
+        // Free-running: they never wait on another GPU, only on the input
+        // ring and (8 chunks back) on the publisher.
+        constexpr int VP = C / kMgProd;
         const int ct = tid - 128;
-        const int cw = ct >> 5;
         unsigned bad = 0;
-        int sti = 0, sta = 0, stb = 0;
-        unsigned phi = 0, pha = 0, phb = 0;
-        int64_t nown = 0;  // owned reduced chunks handed to the publisher
-        bool ok = true, resolved = false;
-        for (int64_t i = 0; ok && i < my_nchunks + kMgLag2; ++i) {
-            if (i < my_nchunks) {
-                // ---- produce chunk i ----
-                const int64_t c = int64_t(blockIdx.x) + i * gridDim.x;
-                const int64_t e0 = c * chunk_elems;
-                const bool fullc = e0 + chunk_elems <= p.n;
-                for (int jj = 0; jj < J; ++jj) {
-                    const int j = p.job_order[jj];
-                    const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
-                    if (!mbar_wait(p, &fin[sti], phi)) {
-                        ok = false;
-                        break;
-                    }
-                    if (p.prof && ct == 0) prof_add(1, clock64() - w0);
-                    const V* r = rows_in + size_t(sti) * 3 * C;
-                    if (fullc)
-                        bad |= loc_item<T, true>(p, s_job[j], j, e0, r, wst, ct);
-                    else
-                        bad |= loc_item<T, false>(p, s_job[j], j, e0, r, wst, ct);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&ein[sti]);
-                    if (++sti == NSI) sti = 0, phi ^= 1u;
+        int sti = 0;
+        unsigned phi = 0;
+        bool ok = true;
+        for (int64_t i = 0; ok && i < my_nchunks; ++i) {
+            const int64_t c = int64_t(blockIdx.x) + i * gridDim.x;
+            const int64_t e0 = c * chunk_elems;
+            const bool fullc = e0 + chunk_elems <= p.n;
+            for (int jj = 0; jj < J; ++jj) {
+                const int j = p.job_order[jj];
+                const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
+                if (!mbar_wait(p, &fin[sti], phi)) {
+                    ok = false;
+                    break;
                 }
-                if (!ok) break;
-                // this GPU's subtree partials (butterfly order inside the subtree)
-                for (int pid = 0; pid < p.n_parts; ++pid) {
+                if (p.prof && ct == 0) prof_add(1, clock64() - w0);
+                const V* r = rows_in + size_t(sti) * 3 * C;
+                if (fullc)
+                    bad |= loc_item<T, true, kMgProd>(p, s_job[j], j, e0, r, wst, ct);
+                else
+                    bad |= loc_item<T, false, kMgProd>(p, s_job[j], j, e0, r, wst, ct);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ein[sti]);
+                if (++sti == NSI) sti = 0, phi ^= 1u;
+            }
+            if (!ok) break;
+            // this GPU's subtree partials (butterfly order inside the subtree)
+            for (int pid = 0; pid < p.n_parts; ++pid) {
 #pragma unroll
-                    for (int kv = 0; kv < kLocVPT; ++kv) {
-                        const int v = kv * kLocConsumers + ct;
-                        const int64_t idx = e0 + int64_t(v) * E;
-                        if (idx >= p.npad) continue;
-                        auto fetch = [&](int leaf) -> V { return wst[s_pjob[pid][leaf] * C + v]; };
-                        __stcg(reinterpret_cast<V*>(s_part[pid] + idx), tree_sum<T>(fetch, s_plog[pid]));
-                    }
-                }
-                // hand the chunk to the publisher (fence + flags off this path)
-                {
-                    const int slot = int(i % kMgPub);
-                    const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
-                    if (i >= kMgPub && !mbar_wait(p, &pk[slot], unsigned(((i / kMgPub) - 1) & 1))) {
-                        ok = false;
-                        break;
-                    }
-                    if (p.prof && ct == 0) prof_add(3, clock64() - w0);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&pd[slot]);
+                for (int kv = 0; kv < VP; ++kv) {
+                    const int v = kv * kMgProd + ct;
+                    const int64_t idx = e0 + int64_t(v) * E;
+                    if (idx >= p.npad) continue;
+                    auto fetch = [&](int leaf) -> V { return wst[s_pjob[pid][leaf] * C + v]; };
+                    __stcg(reinterpret_cast<V*>(s_part[pid] + idx), tree_sum<T>(fetch, s_plog[pid]));
                 }
             }
-            if (!resolved && i >= kMgLag1) {
-                const long long w0 = clock64();
-                while (ready == 0) __nanosleep(32);
-                if (p.prof && ct == 0) prof_add(4, clock64() - w0);
-                __threadfence_block();
-                if (ready != 1) break;
-                resolved = true;
+            // hand the chunk to the publisher (fence + flags off this path)
+            const int slot = int(i % kMgPub);
+            const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
+            if (i >= kMgPub && !mbar_wait(p, &pk[slot], unsigned(((i / kMgPub) - 1) & 1))) {
+                ok = false;
+                break;
             }
-            const int64_t x1 = i - kMgLag1;
-            if (x1 >= 0 && x1 < my_nchunks) {
+            if (p.prof && ct == 0) prof_add(3, clock64() - w0);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pd[slot]);
+        }
+        if (!ok) {
+            if (lane == 0) raise_error(p, WG_ETIMEOUT, blockIdx.x);
+            sm.abort = 1;
+        }
+        report_divergence(p, bad);
+        if (ct == 0) prof_add(0, clock64() - kt0);
+    } else {
+        // ---------------- finishers: phase 1 and phase 2 ----------------
+        constexpr int VF = C / kMgFin;
+        const int ct = tid - 128 - kMgProd;
+        int sta = 0, stb = 0;
+        unsigned pha = 0, phb = 0;
+        int64_t nown = 0;  // owned reduced chunks handed to the publisher
+        bool ok = true;
+        {
+            const long long w0 = clock64();
+            while (ready == 0) __nanosleep(64);
+            __threadfence_block();
+            if (p.prof && ct == 0) prof_add(4, clock64() - w0);
+        }
+        constexpr int kLagB = kMgLag2 - kMgLag1;  // phase 2 trails phase 1 by this many chunks
+        for (int64_t i = 0; ready == 1 && ok && i < my_nchunks + kLagB; ++i) {
+            const int64_t x1 = i;
+            if (x1 < my_nchunks) {
                 // ---- phase 1 of chunk x1 ----
                 const int64_t c = int64_t(blockIdx.x) + x1 * gridDim.x;
                 const int64_t e0 = c * chunk_elems;
@@ -2211,8 +2232,8 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                         if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, x1)]) continue;
                         const DevPlan& P_ = p.plans[pl];
 #pragma unroll
-                        for (int kv = 0; kv < kLocVPT; ++kv) {
-                            const int v = kv * kLocConsumers + ct;
+                        for (int kv = 0; kv < VF; ++kv) {
+                            const int v = kv * kMgFin + ct;
                             const int64_t idx = e0 + int64_t(v) * E;
                             if (idx >= p.npad) continue;
                             auto fetch = [&](int leaf) -> V { return lb[(e + leaf) * C + v]; };
@@ -2241,7 +2262,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                     }
                 }
             }
-            const int64_t x2 = i - kMgLag2;
+            const int64_t x2 = i - kLagB;
             if (x2 >= 0 && x2 < my_nchunks) {
                 // ---- phase 2 of chunk x2: reduced chunks owned elsewhere ----
                 const int64_t c = int64_t(blockIdx.x) + x2 * gridDim.x;
@@ -2259,8 +2280,8 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                         if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, x2)]) continue;
                         const DevPlan& P_ = p.plans[pl];
 #pragma unroll
-                        for (int kv = 0; kv < kLocVPT; ++kv) {
-                            const int v = kv * kLocConsumers + ct;
+                        for (int kv = 0; kv < VF; ++kv) {
+                            const int v = kv * kMgFin + ct;
                             const int64_t idx = e0 + int64_t(v) * E;
                             if (idx >= p.npad) continue;
                             finish_members<T>(p, sm, P_, lb[e * C + v], idx, [&](int j) {
@@ -2279,8 +2300,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
             if (lane == 0) raise_error(p, WG_ETIMEOUT, blockIdx.x);
             sm.abort = 1;
         }
-        report_divergence(p, bad);
-        if (ct == 0) prof_add(0, clock64() - kt0);
+        if (ct == 0) prof_add(14, clock64() - kt0);
     }
     unsigned my_tiles = 0;
     for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x)
