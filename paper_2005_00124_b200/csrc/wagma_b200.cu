@@ -1976,26 +1976,47 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
         }
         __syncwarp();
         const int NSA = s_nsa;
+        // Batches of up to kPullBatch chunks: every lane polls its sources of
+        // the whole batch at once (flag loads of all chunks in flight), one
+        // acquire fence per batch, then the TMA copies.
+        const int B = NSA - 1 < kPullBatch ? (NSA > 1 ? NSA - 1 : 1) : kPullBatch;
         int st = 0;
         unsigned ph = 0;
-        int64_t k = 0;
-        for (int64_t kc = 0; res && kc < my_nchunks; ++kc) {
-            int ra, rb;
-            rows_of(kc, ra, rb);
-            if (!ra) continue;
-            const int64_t c = int64_t(blockIdx.x) + kc * gridDim.x;
+        int64_t k = 0, kc = 0;
+        while (res) {
+            int64_t bk[kPullBatch];
+            int bra[kPullBatch];
+            int nb = 0;
+            while (kc < my_nchunks && nb < B) {
+                int ra, rb;
+                rows_of(kc, ra, rb);
+                if (ra) {
+                    bk[nb] = kc;
+                    bra[nb] = ra;
+                    ++nb;
+                }
+                ++kc;
+            }
+            if (!nb) break;
             const long long w0 = clock64();
-            if (k >= NSA && !mbar_wait(p, &ea[st], ph ^ 1u)) {
+            bool ok = true;
+            for (int b = 0, s2 = st, p2 = int(ph); b < nb && ok; ++b) {
+                if (k + b >= NSA && !mbar_wait(p, &ea[s2], unsigned(p2 ^ 1))) ok = false;
+                if (++s2 == NSA) s2 = 0, p2 ^= 1;
+            }
+            if (!ok) {
                 if (lane == 0) raise_error(p, WG_ETIMEOUT, kc);
                 break;
             }
             const long long w1 = clock64();
-            // wait for every source of the chunk (lane e polls source e), then copy
-            int rc = 0, e = 0;
-            for (int pl = 0; pl < NP; ++pl) {
-                if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, kc)]) continue;
-                for (int u = 0; u < s_ne[pl]; ++u, ++e)
-                    if ((e & 31) == lane && !rc) rc = poll(s_eflag[pl][u], s_estride[pl][u], s_ewant[pl][u], c);
+            int rc = 0, q = 0;
+            for (int b = 0; b < nb; ++b) {
+                const int64_t c = int64_t(blockIdx.x) + bk[b] * gridDim.x;
+                for (int pl = 0; pl < NP; ++pl) {
+                    if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, bk[b])]) continue;
+                    for (int u = 0; u < s_ne[pl]; ++u, ++q)
+                        if ((q & 31) == lane && !rc) rc = poll(s_eflag[pl][u], s_estride[pl][u], s_ewant[pl][u], c);
+                }
             }
             __syncwarp();
             if (lane == 0 && p.prof) {
@@ -2005,19 +2026,30 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
             if (rc) raise_error(p, rc, kc);
             if (__any_sync(0xffffffffu, rc != 0)) break;
             acquire_for_tma();
-            const unsigned cb = pad_bytes(c);
-            if (lane == 0) mbar_arrive_expect_tx(&fa[st], unsigned(ra) * cb);
+            if (lane == 0)
+                for (int b = 0, s2 = st; b < nb; ++b) {
+                    mbar_arrive_expect_tx(&fa[s2], unsigned(bra[b]) * pad_bytes(int64_t(blockIdx.x) + bk[b] * gridDim.x));
+                    if (++s2 == NSA) s2 = 0;
+                }
             __syncwarp();
-            e = 0;
-            for (int pl = 0; pl < NP; ++pl) {
-                if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, kc)]) continue;
-                for (int u = 0; u < s_ne[pl]; ++u, ++e)
-                    if ((e & 31) == lane)
-                        bulk_g2s(rows_a + (size_t(st) * s_rows_a + e) * C, s_esrc[pl][u] + c * chunk_elems, cb, &fa[st]);
+            q = 0;
+            for (int b = 0, s2 = st; b < nb; ++b) {
+                const int64_t c = int64_t(blockIdx.x) + bk[b] * gridDim.x;
+                const unsigned cb = pad_bytes(c);
+                int e = 0;
+                for (int pl = 0; pl < NP; ++pl) {
+                    if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, bk[b])]) continue;
+                    for (int u = 0; u < s_ne[pl]; ++u, ++e, ++q)
+                        if ((q & 31) == lane)
+                            bulk_g2s(rows_a + (size_t(s2) * s_rows_a + e) * C, s_esrc[pl][u] + c * chunk_elems, cb,
+                                     &fa[s2]);
+                }
+                if (++s2 == NSA) s2 = 0;
             }
             __syncwarp();
-            if (++st == NSA) st = 0, ph ^= 1u;
-            ++k;
+            for (int b = 0; b < nb; ++b)
+                if (++st == NSA) st = 0, ph ^= 1u;
+            k += nb;
         }
         if (lane == 0) prof_add(7, clock64() - kt0);
     } else if (warp == 2) {
@@ -2026,41 +2058,71 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
         __threadfence_block();
         if (ready == 1 && s_rows_b) {
             const int NSB = s_nsb;
+            const int B = NSB - 1 < kPullBatch ? (NSB > 1 ? NSB - 1 : 1) : kPullBatch;
             int st = 0;
             unsigned ph = 0;
-            int64_t k = 0;
-            for (int64_t kc = 0; kc < my_nchunks; ++kc) {
-                int ra, rb;
-                rows_of(kc, ra, rb);
-                if (!rb) continue;
-                const int64_t c = int64_t(blockIdx.x) + kc * gridDim.x;
-                if (k >= NSB && !mbar_wait(p, &eb[st], ph ^ 1u)) {
+            int64_t k = 0, kc = 0;
+            for (;;) {
+                int64_t bk[kPullBatch];
+                int brb[kPullBatch];
+                int nb = 0;
+                while (kc < my_nchunks && nb < B) {
+                    int ra, rb;
+                    rows_of(kc, ra, rb);
+                    if (rb) {
+                        bk[nb] = kc;
+                        brb[nb] = rb;
+                        ++nb;
+                    }
+                    ++kc;
+                }
+                if (!nb) break;
+                bool ok = true;
+                for (int b = 0, s2 = st, p2 = int(ph); b < nb && ok; ++b) {
+                    if (k + b >= NSB && !mbar_wait(p, &eb[s2], unsigned(p2 ^ 1))) ok = false;
+                    if (++s2 == NSB) s2 = 0, p2 ^= 1;
+                }
+                if (!ok) {
                     if (lane == 0) raise_error(p, WG_ETIMEOUT, kc);
                     break;
                 }
-                int rc = 0, e = 0;
-                for (int pl = 0; pl < NP; ++pl) {
-                    if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, kc)]) continue;
-                    if ((e & 31) == lane) rc = poll(s_redflag[pl][owner(pl, kc)], 1, s_ver[pl], c);
-                    ++e;
+                int rc = 0, q = 0;
+                for (int b = 0; b < nb; ++b) {
+                    const int64_t c = int64_t(blockIdx.x) + bk[b] * gridDim.x;
+                    for (int pl = 0; pl < NP; ++pl) {
+                        if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, bk[b])]) continue;
+                        if ((q & 31) == lane && !rc) rc = poll(s_redflag[pl][owner(pl, bk[b])], 1, s_ver[pl], c);
+                        ++q;
+                    }
                 }
                 if (rc) raise_error(p, rc, kc);
                 if (__any_sync(0xffffffffu, rc != 0)) break;
                 acquire_for_tma();
-                const unsigned cb = pad_bytes(c);
-                if (lane == 0) mbar_arrive_expect_tx(&fb[st], unsigned(rb) * cb);
+                if (lane == 0)
+                    for (int b = 0, s2 = st; b < nb; ++b) {
+                        mbar_arrive_expect_tx(&fb[s2], unsigned(brb[b]) * pad_bytes(int64_t(blockIdx.x) + bk[b] * gridDim.x));
+                        if (++s2 == NSB) s2 = 0;
+                    }
                 __syncwarp();
-                e = 0;
-                for (int pl = 0; pl < NP; ++pl) {
-                    if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, kc)]) continue;
-                    if ((e & 31) == lane)
-                        bulk_g2s(rows_b + (size_t(st) * s_rows_b + e) * C, s_red[pl][owner(pl, kc)] + c * chunk_elems,
-                                 cb, &fb[st]);
-                    ++e;
+                q = 0;
+                for (int b = 0, s2 = st; b < nb; ++b) {
+                    const int64_t c = int64_t(blockIdx.x) + bk[b] * gridDim.x;
+                    const unsigned cb = pad_bytes(c);
+                    int e = 0;
+                    for (int pl = 0; pl < NP; ++pl) {
+                        if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, bk[b])]) continue;
+                        if ((q & 31) == lane)
+                            bulk_g2s(rows_b + (size_t(s2) * s_rows_b + e) * C, s_red[pl][owner(pl, bk[b])] + c * chunk_elems,
+                                     cb, &fb[s2]);
+                        ++e;
+                        ++q;
+                    }
+                    if (++s2 == NSB) s2 = 0;
                 }
                 __syncwarp();
-                if (++st == NSB) st = 0, ph ^= 1u;
-                ++k;
+                for (int b = 0; b < nb; ++b)
+                    if (++st == NSB) st = 0, ph ^= 1u;
+                k += nb;
             }
         }
     } else if (warp == 3) {
