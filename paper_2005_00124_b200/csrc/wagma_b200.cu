@@ -1704,6 +1704,9 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
 #ifndef WG_MG_IN_STAGES
 #define WG_MG_IN_STAGES 3
 #endif
+#ifndef WG_MG_ACQ_LOAD  // pullers: acquire loads on the flags instead of relaxed loads + fence
+#define WG_MG_ACQ_LOAD 1
+#endif
 #ifndef WG_MG_PUB_BATCH
 #define WG_MG_PUB_BATCH 1
 #endif
@@ -1845,21 +1848,34 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 const int64_t* f = f0 + t * stride + w;
                 const uint64_t tt = globaltimer();
                 int it = 0;
-                int64_t v = ld_relaxed_sys(f);
+                // acquire loads (no fence afterwards: a fence would also wait for
+                // this thread's earlier TMA copies still in flight)
+                auto ld = [&](const int64_t* a) -> int64_t {
+                    if (!WG_MG_ACQ_LOAD) return ld_relaxed_sys(a);
+                    int64_t x;
+                    if (p.fence_scope == 0)
+                        asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(x) : "l"(a) : "memory");
+                    else
+                        asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(x) : "l"(a) : "memory");
+                    return x;
+                };
+                int64_t v = ld(f);
                 while (v < want) {
                     if ((++it & 63) == 0 && (globaltimer() - tt > uint64_t(p.timeout_ns) || aborted(p))) return WG_ETIMEOUT;
                     __nanosleep(32);
-                    v = ld_relaxed_sys(f);
+                    v = ld(f);
                 }
                 if (v >= want + p.D) return WG_EPROTO;
             }
         return 0;
     };
     auto acquire_for_tma = [&]() {
-        if (p.fence_scope == 0)
-            fence_sys();
-        else
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (!WG_MG_ACQ_LOAD) {
+            if (p.fence_scope == 0)
+                fence_sys();
+            else
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
         asm volatile("fence.proxy.async.global;" ::: "memory");
     };
 
