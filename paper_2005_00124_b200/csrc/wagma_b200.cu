@@ -1707,6 +1707,9 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
 #ifndef WG_MG_ACQ_LOAD  // pullers: acquire loads on the flags instead of relaxed loads + fence
 #define WG_MG_ACQ_LOAD 1
 #endif
+#ifndef WG_MG_DIRECT_LOCAL  // this GPU's partials read from L2 by the finishers instead of TMA rows
+#define WG_MG_DIRECT_LOCAL 1
+#endif
 #ifndef WG_MG_PUB_BATCH
 #define WG_MG_PUB_BATCH 1
 #endif
@@ -1754,6 +1757,8 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
     __shared__ T* s_red[kMaxPlans][kMgMaxEff];              // split: reduced-chunk buffer of owner u
     __shared__ int64_t* s_redflag[kMaxPlans][kMgMaxEff];
     __shared__ int8_t s_ownlocal[kMaxPlans][kMgMaxEff];
+    __shared__ int8_t s_erow[kMaxPlans][kMgMaxEff];        // row of the effective leaf in the chunk's rows, -1: read from L2
+    __shared__ int8_t s_nrow[kMaxPlans];
     __shared__ int64_t s_ver[kMaxPlans];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int J = p.n_jobs, NSI = p.loc_stages, NP = p.n_plans;
@@ -1833,7 +1838,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
         ra = rb = 0;
         for (int pl = 0; pl < NP; ++pl) {
             if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, kc)])
-                ra += s_ne[pl];
+                ra += s_nrow[pl];
             else
                 rb += 1;
         }
@@ -1954,6 +1959,12 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                         s_redflag[pl][u] = red_flag_ptr(p, key, 0);
                         s_ownlocal[pl][u] = int8_t(key / p.R == p.gpu_index);
                     }
+                    // this GPU's partials: read by the finishers from L2 (they were
+                    // stored moments ago), only the peers' partials take TMA rows
+                    int nr = 0;
+                    for (int u = 0; u < ne; ++u)
+                        s_erow[pl][u] = (WG_MG_DIRECT_LOCAL && s_ownlocal[pl][u]) ? int8_t(-1) : int8_t(nr++);
+                    s_nrow[pl] = int8_t(nr);
                     s_ne[pl] = int8_t(ne);
                     s_elog[pl] = int8_t(P_.log_leaves - hl);
                     s_mode[pl] = (p.mg_split && split_pays(ne, __popc(gpus))) ? kMgSplit : kMgHier;
@@ -1967,12 +1978,14 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                         s_estride[pl][li] = kWarps;
                         s_ewant[pl][li] = sm.leaf_src[pl][li] == kSrcReady ? kNever : st;
                         s_ownlocal[pl][li] = 1;
+                        s_erow[pl][li] = int8_t(li);
                     }
+                    s_nrow[pl] = int8_t(P_.n_leaves);
                     s_ne[pl] = int8_t(P_.n_leaves);
                     s_elog[pl] = int8_t(P_.log_leaves);
                     s_mode[pl] = kMgPull;
                 }
-                ra_max += s_ne[pl];
+                ra_max += s_nrow[pl];
                 rb_max += s_mode[pl] == kMgSplit;
             }
             s_rows_a = ra_max;
@@ -2055,10 +2068,14 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 int e = 0;
                 for (int pl = 0; pl < NP; ++pl) {
                     if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, bk[b])]) continue;
-                    for (int u = 0; u < s_ne[pl]; ++u, ++e, ++q)
+                    for (int u = 0; u < s_ne[pl]; ++u) {
+                        if (s_erow[pl][u] < 0) continue;
                         if ((q & 31) == lane)
                             bulk_g2s(rows_a + (size_t(s2) * s_rows_a + e) * C, s_esrc[pl][u] + c * chunk_elems, cb,
                                      &fa[s2]);
+                        ++e;
+                        ++q;
+                    }
                 }
                 if (++s2 == NSA) s2 = 0;
             }
@@ -2314,7 +2331,11 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                             const int v = kv * kMgFin + ct;
                             const int64_t idx = e0 + int64_t(v) * E;
                             if (idx >= p.npad) continue;
-                            auto fetch = [&](int leaf) -> V { return lb[(e + leaf) * C + v]; };
+                            auto fetch = [&](int leaf) -> V {
+                                const int row = s_erow[pl][leaf];
+                                if (row >= 0) return lb[(e + row) * C + v];
+                                return __ldcg(reinterpret_cast<const V*>(s_esrc[pl][leaf] + idx));
+                            };
                             const V acc = tree_sum<T>(fetch, s_elog[pl]);
                             if (s_mode[pl] == kMgSplit)  // the owner's reduced chunk, for the other members
                                 __stcg(reinterpret_cast<V*>(s_red[pl][owner(pl, x1)] + idx), acc);
@@ -2323,7 +2344,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                             });
                         }
                         owned = owned || s_mode[pl] == kMgSplit;
-                        e += s_ne[pl];
+                        e += s_nrow[pl];
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&ea[sta]);
