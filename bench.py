@@ -377,6 +377,18 @@ def run_ours(a):
     clocks = sampler.stop() if sampler else None
     gpu_launches = ctx.launches - launches0
     ctx.check()
+    # contribution stamps the activation protocol locked for the last timed
+    # versions (descriptor ring): how many contributions were stale
+    stale = total_c = 0
+    from paper_2005_00124_b200.optim import is_sync_iteration
+    for v in range(max(t_first, t - ctx.ring_depth + 1), t):
+        if is_sync_iteration(v, a.tau) or a.blocking:
+            continue
+        stamps, locked = ctx.query_version(v)
+        if locked:
+            total_c += len(stamps)
+            stale += sum(1 for st in stamps if st != v)
+    protocol = {"stale_contributions": stale, "contributions": total_c}
     elapsed_ms = allmax(start.elapsed_time(end))
     kern_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(a.steps)]
     kern_avg_ms = allmax(sum(kern_ms) / len(kern_ms))
@@ -495,7 +507,7 @@ def run_ours(a):
                 "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": a.dtype, "data": "synthetic", "config": config_dict(a, G),
                 "group_avg_gbs": group_avg_gbs, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": gpu_launches, "clocks": clocks,
+                "gpu_launches": gpu_launches, "clocks": clocks, "protocol_last_versions": protocol,
                 "replicas_after_sync": {"iteration": t - 1, "bit_identical": diag.identical, "gamma": diag.gamma}}
         if a.blocking or a.victims or a.base_ms or a.length_buckets or a.fixed_victim >= 0:
             from paper_2005_00124_b200.optim import is_sync_iteration

@@ -443,19 +443,17 @@ __device__ void control_phase(const LaunchParams& p, int* s_activator) {
         }
         // Bounded grace window: ranks on other GPUs that join within it are
         // timely. Ranks on this GPU announced at launch start (final).
-        // Adaptive: a rank that was late for the previous version (a
-        // straggler) is not waited for, so a persistent straggler does not
-        // cost every version the whole window; it is still timely if it
-        // announces before the lock.
+        // Adaptive: a rank that has not even announced version v-1 is at
+        // least a whole version behind (a straggler): it is not waited for,
+        // so a persistent straggler does not cost every version the whole
+        // window (it is still timely if it announces before the lock). A
+        // rank slightly behind (it announced v-1) is waited for as usual.
         const uint64_t t0 = globaltimer();
         const int q0 = lane, q1 = lane + 32;
         bool skip0 = false, skip1 = false;
-        if (p.adaptive_grace && v >= 1) {
-            const Desc* dp = desc_ptr(p, v - 1);
-            if (ld_acquire_sys(&dp->state) == v * 4 + 2) {  // version v-1 locked (a live version)
-                skip0 = q0 < p.P && ld_relaxed_sys(&dp->stamps[q0]) < v - 1;
-                skip1 = q1 < p.P && ld_relaxed_sys(&dp->stamps[q1]) < v - 1;
-            }
+        if (p.adaptive_grace) {
+            skip0 = q0 < p.P && ld_acquire_sys(announce_ptr(p, q0)) < v - 1;
+            skip1 = q1 < p.P && ld_acquire_sys(announce_ptr(p, q1)) < v - 1;
         }
         int64_t a0 = kNever, a1 = kNever;
         for (;;) {
