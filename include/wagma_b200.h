@@ -37,6 +37,8 @@ extern "C" {
 #define WG_ECUDA 6
 #define WG_ENOMEM 7
 #define WG_EDIVERGE 8 /* non-finite W' produced (gradient or replica); optim.DivergenceError */
+#define WG_ESYNC 9    /* mismatched sync points: a rank joined iteration t as a global sync while another
+                         joined it as a group round (collective.py:381-386); collective.ProtocolFault */
 
 #define WG_RULE_EXAMPLE 0 /* topology.MASK_RULE_EXAMPLE ("example") */
 #define WG_RULE_LITERAL 1 /* topology.MASK_RULE_LITERAL ("literal") */

@@ -12,7 +12,8 @@ import os
 
 from . import _build
 
-WG_OK, WG_EINVAL, WG_EVERSION, WG_ESTALE, WG_EPROTO, WG_ETIMEOUT, WG_ECUDA, WG_ENOMEM, WG_EDIVERGE = range(9)
+(WG_OK, WG_EINVAL, WG_EVERSION, WG_ESTALE, WG_EPROTO, WG_ETIMEOUT, WG_ECUDA, WG_ENOMEM, WG_EDIVERGE,
+ WG_ESYNC) = range(10)
 WG_RULE_EXAMPLE, WG_RULE_LITERAL = 0, 1
 WG_F32, WG_F64 = 0, 1
 WG_JOB_STEP, WG_JOB_SYNC_STEP, WG_JOB_LOCAL_STEP, WG_JOB_GROUP_SUM, WG_JOB_SYNC_SUM = range(5)

@@ -122,9 +122,9 @@ def _submit(ctx: DeviceContext, job: Job, resolve: Callable) -> None:
 def _run(ctx: DeviceContext, items: list[_Pending]) -> None:
     if not items:
         return
-    ctx.launch([it.job for it in items])
-    torch.cuda.current_stream(ctx.torch_device).synchronize()
     try:
+        ctx.launch([it.job for it in items])
+        torch.cuda.current_stream(ctx.torch_device).synchronize()
         ctx.check()
     except DeviceProtocolFault as exc:
         ctx.clear_error()

@@ -171,6 +171,8 @@ class DeviceContext:
         msg = f"{what}: {self.lib.wg_strerror(rc).decode()} ({_lib.last_error()})"
         if rc == _lib.WG_EINVAL:
             raise InvalidParamsError(msg)
+        if rc in (_lib.WG_EVERSION, _lib.WG_ESTALE, _lib.WG_EPROTO, _lib.WG_ESYNC):
+            raise DeviceProtocolFault(rc, -1, msg)
         raise RuntimeError(msg)
 
     def error(self) -> tuple[int, int]:

@@ -82,6 +82,7 @@ struct Layout {
     int64_t announce;  // int64 [R] (128-byte stride): latest announced version
     int64_t complete;  // int64 [R][D]: stamp whose tiles are all published
     int64_t counter;   // uint32 [R][D]: tiles published for the current stamp
+    int64_t syncmark;  // int64 [R][D]: 2(v+1) + (v joined as a global sync) of the stamp v in the slot, 0 never
     int64_t desc;      // Desc [Dv]  (used on GPU 0 only)
     int64_t flags;     // int64 [R][n_tiles][warps]: latest stamp published per warp-tile
     int64_t ring;      // T [R][D][npad]: send ring
@@ -308,6 +309,9 @@ __device__ __forceinline__ int slot_of(const LaunchParams& p, int64_t stamp) {
 __device__ __forceinline__ int64_t* complete_ptr(const LaunchParams& p, int rank, int slot) {
     return reinterpret_cast<int64_t*>(rank_base(p, rank) + p.L.complete) + (rank % p.R) * p.D + slot;
 }
+__device__ __forceinline__ int64_t* syncmark_ptr(const LaunchParams& p, int rank, int slot) {
+    return reinterpret_cast<int64_t*>(rank_base(p, rank) + p.L.syncmark) + (rank % p.R) * p.D + slot;
+}
 __device__ __forceinline__ unsigned* counter_ptr(const LaunchParams& p, int rank, int slot) {
     return reinterpret_cast<unsigned*>(rank_base(p, rank) + p.L.counter) + (rank % p.R) * p.D + slot;
 }
@@ -401,8 +405,15 @@ __device__ void control_phase(const LaunchParams& p, int* s_activator) {
     // Announce "rank r is producing W'_v in a running kernel" (the join,
     // collective.py:192-205). Activators lock contribution stamps from it.
     if (lane == 0) {
-        for (int j = 0; j < p.n_jobs; ++j)
-            if (p.jobs[j].produces) st_release_sys(announce_ptr(p, p.jobs[j].rank), p.jobs[j].version);
+        for (int j = 0; j < p.n_jobs; ++j) {
+            const DevJob& jb = p.jobs[j];
+            if (!jb.produces) continue;
+            // how this rank joins version v (global sync or group round): the
+            // sync-point check of every consumer (check_sync_points)
+            st_relaxed_sys(syncmark_ptr(p, jb.rank, slot_of(p, jb.version)),
+                           2 * (jb.version + 1) + (p.versions[jb.vidx].mode == kSync));
+            st_release_sys(announce_ptr(p, jb.rank), jb.version);
+        }
         fence_sys();
     }
     __syncwarp();
@@ -513,6 +524,39 @@ struct SmemCtl {
     int32_t activator[kMaxVersions];
     int32_t abort;
 };
+
+// Sync-point agreement (collective.py:381-386: "mismatched sync points"), one
+// warp of CTA 0 after the launch consumed its leaves. Every rank marks how it
+// joins each version (control_phase: 2(v+1), +1 for a global sync):
+//  - a global sync at v needs every rank to have joined v as a sync (its W'_v
+//    was consumed, so its mark is on the way);
+//  - a group round at v must not see a timely member that joined v as a sync.
+// Either mismatch latches WG_ESYNC (info v * 1024 + rank), a ProtocolFault.
+__device__ void check_sync_points(const LaunchParams& p, const SmemCtl& sm) {
+    const int lane = threadIdx.x & 31;
+    if (sm.abort) return;
+    for (int vi = 0; vi < p.n_versions; ++vi) {
+        const int64_t v = p.versions[vi].version;
+        const bool sync = p.versions[vi].mode == kSync;
+        const int slot = slot_of(p, v);
+        for (int q = lane; q < p.P; q += 32) {
+            const int64_t* mk = syncmark_ptr(p, q, slot);
+            int64_t x = ld_acquire_sys(mk);
+            if (sync) {
+                const uint64_t t0 = globaltimer();
+                int it = 0;
+                while (x < 2 * (v + 1)) {
+                    if ((++it & 63) == 0 && (globaltimer() - t0 > uint64_t(p.timeout_ns) || aborted(p))) break;
+                    __nanosleep(64);
+                    x = ld_acquire_sys(mk);
+                }
+                if (x == 2 * (v + 1)) raise_error(p, WG_ESYNC, v * 1024 + q);
+            } else if (sm.stamps[vi][q] == v && x == 2 * (v + 1) + 1) {
+                raise_error(p, WG_ESYNC, v * 1024 + q);
+            }
+        }
+    }
+}
 
 // Resolve every plan's leaves to a source (after lock-in), executed by
 // `nthr` threads starting at thread index `t0` (the whole CTA, or one warp)
@@ -1099,6 +1143,8 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
     if (blockIdx.x == 0) {
         if (!resolved && !sm.abort) resolved = resolve_sources<T>(p, sm);
         __syncthreads();
+        if (resolved && threadIdx.x < 32) check_sync_points(p, sm);
+        __syncthreads();
         if (threadIdx.x < p.n_jobs) {
             const DevJob& jb = p.jobs[threadIdx.x];
             wg_job_status st;
@@ -1185,6 +1231,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
     unsigned ok;
     asm volatile(
         "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n selp.u32 %0, 1, 0, q;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Non-blocking test of an mbarrier phase (try_wait may suspend the thread
+// for a while; a warp polling several barriers must not).
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred q;\n mbarrier.test_wait.parity.shared::cta.b64 q, [%1], %2;\n selp.u32 %0, 1, 0, q;\n}\n"
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
@@ -1657,6 +1714,8 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
     if (blockIdx.x == 0) {
         __syncthreads();
         const bool res = ready == 1;
+        if (res && threadIdx.x < 32) check_sync_points(p, sm);
+        __syncthreads();
         if (tid < p.n_jobs) {
             const DevJob& jb = p.jobs[tid];
             wg_job_status stt;
@@ -1699,14 +1758,8 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
 #ifndef WG_MG_LAG2
 #define WG_MG_LAG2 4
 #endif
-#ifndef WG_MG_IN_STAGES
-#define WG_MG_IN_STAGES 3
-#endif
-#ifndef WG_MG_ACQ_LOAD  // pullers: acquire loads on the flags instead of relaxed loads + fence
-#define WG_MG_ACQ_LOAD 1
-#endif
-#ifndef WG_MG_DIRECT_LOCAL  // this GPU's partials read from L2 by the finishers instead of TMA rows
-#define WG_MG_DIRECT_LOCAL 1
+#ifndef WG_MG_IN_STAGES_MAX  // deepest input ring tried (the launch takes the deepest that fits)
+#define WG_MG_IN_STAGES_MAX 5
 #endif
 #ifndef WG_MG_PUB_BATCH
 #define WG_MG_PUB_BATCH 1
@@ -1721,8 +1774,9 @@ constexpr int kMgPubBatch = WG_MG_PUB_BATCH;  // chunks published per fence (< k
 #endif
 constexpr int kMgProd = WG_MG_PROD_WARPS * 32;  // producer threads (W', partials)
 constexpr int kMgFin = WG_MG_FIN_WARPS * 32;    // finisher threads (phase 1 and 2)
-// + input TMA warp, control/phase-1 puller, phase-2 puller, publisher
-constexpr int kMgThreads = 128 + kMgProd + kMgFin;
+// role warps: input TMA, control/phase-1 puller, phase-2 puller, publisher
+constexpr int kMgRoleWarps = 4;
+constexpr int kMgThreads = kMgRoleWarps * 32 + kMgProd + kMgFin;
 constexpr int kMgPub = 8;                         // chunks in flight between the consumers and the publisher
 constexpr int kMgMaxEff = 16;                   // effective leaves per plan
 enum MgMode : int8_t { kMgPull = 0, kMgHier = 1, kMgSplit = 2 };
@@ -1831,55 +1885,140 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
     };
     // owner (effective-leaf index) of chunk kc of a split plan
     auto owner = [&](int pl, int64_t kc) -> int { return int(kc % s_ne[pl]); };
-    // phase-1 / phase-2 rows of CTA-local chunk kc (identical in pullers and consumers)
-    auto rows_of = [&](int64_t kc, int& ra, int& rb) {
-        ra = rb = 0;
+    auto c_of = [&](int64_t kc) -> int64_t { return int64_t(blockIdx.x) + kc * gridDim.x; };
+    // phase 1 of plan pl on CTA-local chunk kc (everything but split chunks owned elsewhere)
+    auto ph1 = [&](int pl, int64_t kc) -> bool { return s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, kc)]; };
+    // phase-1 TMA rows of chunk kc (-1: no phase 1), phase-2 rows (-1: none)
+    auto rows_a_of = [&](int64_t kc) -> int {
+        int ra = -1;
+        for (int pl = 0; pl < NP; ++pl)
+            if (ph1(pl, kc)) ra = (ra < 0 ? 0 : ra) + s_nrow[pl];
+        return ra;
+    };
+    auto rows_b_of = [&](int64_t kc) -> int {
+        int rb = 0;
+        for (int pl = 0; pl < NP; ++pl) rb += !ph1(pl, kc);
+        return rb ? rb : -1;
+    };
+    // phase-1 sources of chunk kc in a fixed order: visit(flag, stride, want, src, row or -1)
+    auto srcs_a = [&](int64_t kc, auto&& visit) {
+        int e = 0;
         for (int pl = 0; pl < NP; ++pl) {
-            if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, kc)])
-                ra += s_nrow[pl];
-            else
-                rb += 1;
+            if (!ph1(pl, kc)) continue;
+            for (int u = 0; u < s_ne[pl]; ++u)
+                visit(s_eflag[pl][u], int(s_estride[pl][u]), s_ewant[pl][u], s_esrc[pl][u],
+                      s_erow[pl][u] >= 0 ? e + s_erow[pl][u] : -1);
+            e += s_nrow[pl];
         }
     };
-    // wait for flags >= want of one effective source over the chunk's tiles
-    auto poll = [&](const int64_t* f0, int stride, int64_t want, int64_t c) -> int {
-        if (want == kNever) return 0;  // a completed older slot (checked at resolve)
+    // phase-2 sources: the owners' reduced chunks
+    auto srcs_b = [&](int64_t kc, auto&& visit) {
+        int e = 0;
+        for (int pl = 0; pl < NP; ++pl) {
+            if (ph1(pl, kc)) continue;
+            const int o = owner(pl, kc);
+            visit(static_cast<const int64_t*>(s_redflag[pl][o]), 1, s_ver[pl], static_cast<const T*>(s_red[pl][o]), e++);
+        }
+    };
+    // One non-blocking look at the flags >= want of one source over chunk c's
+    // tiles (acquire loads): 1 ready, 0 not yet, -code on a protocol fault.
+    auto probe = [&](const int64_t* f0, int stride, int64_t want, int64_t c) -> int {
+        if (want == kNever) return 1;  // a completed older slot (checked at resolve)
         const int64_t t0 = c * kLocTiles;
-        const int64_t nt = p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles;
-        for (int64_t t = t0; t < t0 + nt; ++t)
+        const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
+        int ready = 1;
+        for (int t = 0; t < nt; ++t)
             for (int w = 0; w < stride; ++w) {
-                const int64_t* f = f0 + t * stride + w;
-                const uint64_t tt = globaltimer();
-                int it = 0;
-                // acquire loads (no fence afterwards: a fence would also wait for
-                // this thread's earlier TMA copies still in flight)
-                auto ld = [&](const int64_t* a) -> int64_t {
-                    if (!WG_MG_ACQ_LOAD) return ld_relaxed_sys(a);
-                    int64_t x;
-                    if (p.fence_scope == 0)
-                        asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(x) : "l"(a) : "memory");
-                    else
-                        asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(x) : "l"(a) : "memory");
-                    return x;
-                };
-                int64_t v = ld(f);
-                while (v < want) {
-                    if ((++it & 63) == 0 && (globaltimer() - tt > uint64_t(p.timeout_ns) || aborted(p))) return WG_ETIMEOUT;
-                    __nanosleep(32);
-                    v = ld(f);
-                }
-                if (v >= want + p.D) return WG_EPROTO;
+                const int64_t* a = f0 + (t0 + t) * stride + w;
+                int64_t x;
+                if (p.fence_scope == 0)
+                    asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(x) : "l"(a) : "memory");
+                else
+                    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(x) : "l"(a) : "memory");
+                if (x < want) ready = 0;
+                else if (x >= want + p.D) return -WG_EPROTO;
             }
-        return 0;
+        return ready;
     };
-    auto acquire_for_tma = [&]() {
-        if (!WG_MG_ACQ_LOAD) {
-            if (p.fence_scope == 0)
-                fence_sys();
-            else
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    // Sliding-window puller (warps 1 and 2). Chunks in CTA order; source q
+    // of a chunk belongs to lane q % 32, which probes its flags and, once
+    // every lane has seen all its flags of that chunk and of every earlier
+    // one, issues its TMA row copy. A chunk is never held back by a later
+    // chunk's flags: on another GPU a later chunk may wait, through its
+    // owner's reduce, on this GPU consuming the earlier one (no wait cycle).
+    auto puller = [&](int NS, V* rows, int rows_per_stage, uint64_t* full, uint64_t* empty, auto&& nrows,
+                      auto&& srcs) -> bool {
+        const int W = NS < kPullBatch ? NS : kPullBatch;  // chunks whose flags are probed together
+        int st = 0;
+        unsigned ph = 0;
+        int64_t k = 0, kc = 0;
+        for (;;) {
+            int64_t bk[kPullBatch];
+            int nb = 0;
+            while (kc < my_nchunks && nb < W) {
+                if (nrows(kc) >= 0) bk[nb++] = kc;
+                ++kc;
+            }
+            if (!nb) return true;
+            int lane_b = 0, done = 0, spins = 0;
+            const uint64_t t0 = globaltimer();
+            while (done < nb) {
+                int rc = 0;
+                while (lane_b < nb && !rc) {
+                    bool all = true;
+                    int q = 0;
+                    const int64_t c = c_of(bk[lane_b]);
+                    srcs(bk[lane_b], [&](const int64_t* f, int stride, int64_t want, const T*, int) {
+                        if ((q++ & 31) != lane || !all || rc) return;
+                        const int r = probe(f, stride, want, c);
+                        if (r < 0)
+                            rc = -r;
+                        else if (r == 0)
+                            all = false;
+                    });
+                    if (!all) break;
+                    if (!rc) ++lane_b;
+                }
+                if (rc) raise_error(p, rc, bk[lane_b]);
+                if (__any_sync(0xffffffffu, rc != 0)) return false;
+                const int rdy = __reduce_min_sync(0xffffffffu, lane_b);
+                if (rdy == done) {
+                    if ((++spins & 63) == 0 && (globaltimer() - t0 > uint64_t(p.timeout_ns) || aborted(p))) {
+                        if (lane == 0) raise_error(p, WG_ETIMEOUT, bk[done]);
+                        return false;
+                    }
+                    __nanosleep(32);
+                    continue;
+                }
+                // the flags were read with acquire loads; order them before the
+                // async-proxy (TMA) reads of the data they guard
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                for (int b = done; b < rdy; ++b, ++k) {
+                    if (k >= NS && !mbar_wait(p, &empty[st], ph ^ 1u)) {
+                        if (lane == 0) raise_error(p, WG_ETIMEOUT, bk[b]);
+                        return false;
+                    }
+                    const int64_t c = c_of(bk[b]);
+                    const unsigned cb = pad_bytes(c);
+                    if (lane == 0) mbar_arrive_expect_tx(&full[st], unsigned(nrows(bk[b])) * cb);
+                    __syncwarp();
+                    int q = 0;
+                    srcs(bk[b], [&](const int64_t*, int, int64_t, const T* src, int row) {
+                        if ((q++ & 31) == lane && row >= 0)
+                            bulk_g2s(rows + (size_t(st) * rows_per_stage + row) * C, src + c * chunk_elems, cb, &full[st]);
+                    });
+                    __syncwarp();
+                    if (++st == NS) st = 0, ph ^= 1u;
+                }
+                done = rdy;
+            }
         }
-        asm volatile("fence.proxy.async.global;" ::: "memory");
+    };
+    auto fence_pub = [&]() {
+        if (p.fence_scope == 0)
+            fence_sys();
+        else if (p.fence_scope == 1)
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
     };
 
     if (warp == 0) {
@@ -1942,6 +2081,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 s_ver[pl] = v;
                 bool hier = p.plan_hl[pl] > 0;
                 for (int li = 0; li < P_.n_leaves && hier; ++li) hier = sm.stamps[P_.vidx][P_.leaves[li]] == v;
+                int nr = 0;
                 if (hier) {
                     const int hl = p.plan_hl[pl];
                     const int ne = P_.n_leaves >> hl;
@@ -1956,18 +2096,16 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                         s_red[pl][u] = red_ptr<T>(p, key, v);
                         s_redflag[pl][u] = red_flag_ptr(p, key, 0);
                         s_ownlocal[pl][u] = int8_t(key / p.R == p.gpu_index);
+                        // this GPU's partials: read by the finishers from L2 (stored
+                        // moments ago); only the peers' partials take TMA rows
+                        s_erow[pl][u] = s_ownlocal[pl][u] ? int8_t(-1) : int8_t(nr++);
                     }
-                    // this GPU's partials: read by the finishers from L2 (they were
-                    // stored moments ago), only the peers' partials take TMA rows
-                    int nr = 0;
-                    for (int u = 0; u < ne; ++u)
-                        s_erow[pl][u] = (WG_MG_DIRECT_LOCAL && s_ownlocal[pl][u]) ? int8_t(-1) : int8_t(nr++);
-                    s_nrow[pl] = int8_t(nr);
                     s_ne[pl] = int8_t(ne);
                     s_elog[pl] = int8_t(P_.log_leaves - hl);
                     s_mode[pl] = (p.mg_split && split_pays(ne, __popc(gpus))) ? kMgSplit : kMgHier;
                 } else {
-                    // leaf pull (a member is stale): every leaf's send slot
+                    // leaf pull (a member is stale): every leaf's send slot; this
+                    // GPU's leaves are read from L2 / HBM, the peers' by TMA
                     for (int li = 0; li < P_.n_leaves; ++li) {
                         const int q = P_.leaves[li];
                         const int64_t st = sm.stamps[P_.vidx][q];
@@ -1976,17 +2114,17 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                         s_estride[pl][li] = kWarps;
                         s_ewant[pl][li] = sm.leaf_src[pl][li] == kSrcReady ? kNever : st;
                         s_ownlocal[pl][li] = 1;
-                        s_erow[pl][li] = int8_t(li);
+                        s_erow[pl][li] = q / p.R == p.gpu_index ? int8_t(-1) : int8_t(nr++);
                     }
-                    s_nrow[pl] = int8_t(P_.n_leaves);
                     s_ne[pl] = int8_t(P_.n_leaves);
                     s_elog[pl] = int8_t(P_.log_leaves);
                     s_mode[pl] = kMgPull;
                 }
+                s_nrow[pl] = int8_t(nr);
                 ra_max += s_nrow[pl];
                 rb_max += s_mode[pl] == kMgSplit;
             }
-            s_rows_a = ra_max;
+            s_rows_a = ra_max > 0 ? ra_max : 1;
             s_rows_b = rb_max;
             s_nsa = ra_max ? (p.mg_cap_a / ra_max < kMgMaxStagesA ? p.mg_cap_a / ra_max : kMgMaxStagesA) : kMgMaxStagesA;
             s_nsb = rb_max ? (p.mg_cap_b / rb_max < kMgMaxStagesB ? p.mg_cap_b / rb_max : kMgMaxStagesB) : kMgMaxStagesB;
@@ -2002,245 +2140,123 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
             prof_add(11, clock64() - kt0);
         }
         __syncwarp();
-        const int NSA = s_nsa;
-        // Batches of up to kPullBatch chunks: every lane polls its sources of
-        // the whole batch at once (flag loads of all chunks in flight), one
-        // acquire fence per batch, then the TMA copies.
-        const int B = NSA - 1 < kPullBatch ? (NSA > 1 ? NSA - 1 : 1) : kPullBatch;
-        int st = 0;
-        unsigned ph = 0;
-        int64_t k = 0, kc = 0;
-        while (res) {
-            int64_t bk[kPullBatch];
-            int bra[kPullBatch];
-            int nb = 0;
-            while (kc < my_nchunks && nb < B) {
-                int ra, rb;
-                rows_of(kc, ra, rb);
-                if (ra) {
-                    bk[nb] = kc;
-                    bra[nb] = ra;
-                    ++nb;
-                }
-                ++kc;
-            }
-            if (!nb) break;
-            const long long w0 = clock64();
-            bool ok = true;
-            for (int b = 0, s2 = st, p2 = int(ph); b < nb && ok; ++b) {
-                if (k + b >= NSA && !mbar_wait(p, &ea[s2], unsigned(p2 ^ 1))) ok = false;
-                if (++s2 == NSA) s2 = 0, p2 ^= 1;
-            }
-            if (!ok) {
-                if (lane == 0) raise_error(p, WG_ETIMEOUT, kc);
-                break;
-            }
-            const long long w1 = clock64();
-            int rc = 0, q = 0;
-            for (int b = 0; b < nb; ++b) {
-                const int64_t c = int64_t(blockIdx.x) + bk[b] * gridDim.x;
-                for (int pl = 0; pl < NP; ++pl) {
-                    if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, bk[b])]) continue;
-                    for (int u = 0; u < s_ne[pl]; ++u, ++q)
-                        if ((q & 31) == lane && !rc) rc = poll(s_eflag[pl][u], s_estride[pl][u], s_ewant[pl][u], c);
-                }
-            }
-            __syncwarp();
-            if (lane == 0 && p.prof) {
-                prof_add(6, w1 - w0);
-                prof_add(5, clock64() - w1);
-            }
-            if (rc) raise_error(p, rc, kc);
-            if (__any_sync(0xffffffffu, rc != 0)) break;
-            acquire_for_tma();
-            if (lane == 0)
-                for (int b = 0, s2 = st; b < nb; ++b) {
-                    mbar_arrive_expect_tx(&fa[s2], unsigned(bra[b]) * pad_bytes(int64_t(blockIdx.x) + bk[b] * gridDim.x));
-                    if (++s2 == NSA) s2 = 0;
-                }
-            __syncwarp();
-            q = 0;
-            for (int b = 0, s2 = st; b < nb; ++b) {
-                const int64_t c = int64_t(blockIdx.x) + bk[b] * gridDim.x;
-                const unsigned cb = pad_bytes(c);
-                int e = 0;
-                for (int pl = 0; pl < NP; ++pl) {
-                    if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, bk[b])]) continue;
-                    for (int u = 0; u < s_ne[pl]; ++u) {
-                        if (s_erow[pl][u] < 0) continue;
-                        if ((q & 31) == lane)
-                            bulk_g2s(rows_a + (size_t(s2) * s_rows_a + e) * C, s_esrc[pl][u] + c * chunk_elems, cb,
-                                     &fa[s2]);
-                        ++e;
-                        ++q;
-                    }
-                }
-                if (++s2 == NSA) s2 = 0;
-            }
-            __syncwarp();
-            for (int b = 0; b < nb; ++b)
-                if (++st == NSA) st = 0, ph ^= 1u;
-            k += nb;
-        }
+        if (res) puller(s_nsa, rows_a, s_rows_a, fa, ea, rows_a_of, srcs_a);
         if (lane == 0) prof_add(7, clock64() - kt0);
     } else if (warp == 2) {
         // ---------------- phase-2 puller: owners' reduced chunks ----------------
         while (ready == 0) __nanosleep(64);
         __threadfence_block();
-        if (ready == 1 && s_rows_b) {
-            const int NSB = s_nsb;
-            const int B = NSB - 1 < kPullBatch ? (NSB > 1 ? NSB - 1 : 1) : kPullBatch;
-            int st = 0;
-            unsigned ph = 0;
-            int64_t k = 0, kc = 0;
-            for (;;) {
-                int64_t bk[kPullBatch];
-                int brb[kPullBatch];
-                int nb = 0;
-                while (kc < my_nchunks && nb < B) {
-                    int ra, rb;
-                    rows_of(kc, ra, rb);
-                    if (rb) {
-                        bk[nb] = kc;
-                        brb[nb] = rb;
-                        ++nb;
-                    }
-                    ++kc;
-                }
-                if (!nb) break;
-                bool ok = true;
-                for (int b = 0, s2 = st, p2 = int(ph); b < nb && ok; ++b) {
-                    if (k + b >= NSB && !mbar_wait(p, &eb[s2], unsigned(p2 ^ 1))) ok = false;
-                    if (++s2 == NSB) s2 = 0, p2 ^= 1;
-                }
-                if (!ok) {
-                    if (lane == 0) raise_error(p, WG_ETIMEOUT, kc);
-                    break;
-                }
-                int rc = 0, q = 0;
-                for (int b = 0; b < nb; ++b) {
-                    const int64_t c = int64_t(blockIdx.x) + bk[b] * gridDim.x;
-                    for (int pl = 0; pl < NP; ++pl) {
-                        if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, bk[b])]) continue;
-                        if ((q & 31) == lane && !rc) rc = poll(s_redflag[pl][owner(pl, bk[b])], 1, s_ver[pl], c);
-                        ++q;
-                    }
-                }
-                if (rc) raise_error(p, rc, kc);
-                if (__any_sync(0xffffffffu, rc != 0)) break;
-                acquire_for_tma();
-                if (lane == 0)
-                    for (int b = 0, s2 = st; b < nb; ++b) {
-                        mbar_arrive_expect_tx(&fb[s2], unsigned(brb[b]) * pad_bytes(int64_t(blockIdx.x) + bk[b] * gridDim.x));
-                        if (++s2 == NSB) s2 = 0;
-                    }
-                __syncwarp();
-                q = 0;
-                for (int b = 0, s2 = st; b < nb; ++b) {
-                    const int64_t c = int64_t(blockIdx.x) + bk[b] * gridDim.x;
-                    const unsigned cb = pad_bytes(c);
-                    int e = 0;
-                    for (int pl = 0; pl < NP; ++pl) {
-                        if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, bk[b])]) continue;
-                        if ((q & 31) == lane)
-                            bulk_g2s(rows_b + (size_t(s2) * s_rows_b + e) * C, s_red[pl][owner(pl, bk[b])] + c * chunk_elems,
-                                     cb, &fb[s2]);
-                        ++e;
-                        ++q;
-                    }
-                    if (++s2 == NSB) s2 = 0;
-                }
-                __syncwarp();
-                for (int b = 0; b < nb; ++b)
-                    if (++st == NSB) st = 0, ph ^= 1u;
-                k += nb;
-            }
-        }
+        if (ready == 1 && s_rows_b) puller(s_nsb, rows_b, s_rows_b, fb, eb, rows_b_of, srcs_b);
     } else if (warp == 3) {
         // ---------------- publisher: fences and readiness flags ----------------
-        // Walks the consumers' sequence (produce i, then phase 1 of i - lag):
-        // waits for every consumer warp's arrival, issues one fence
-        // (cumulative over their stores, acquired through the mbarrier) and
-        // raises the flags, so no consumer ever waits on a fence.
-        auto fence_pub = [&]() {
-            if (p.fence_scope == 0)
-                fence_sys();
-            else if (p.fence_scope == 1)
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        };
-        int64_t nown = 0;
-        bool res = true;
-        for (int64_t i = 0; res && i < my_nchunks + kMgLag1; ++i) {
-            if (i < my_nchunks) {
-                const int slot = int(i % kMgPub);
-                const long long w0 = clock64();
-                if (!mbar_wait(p, &pd[slot], unsigned((i / kMgPub) & 1))) break;
-                // chunks are published in batches of kMgPubBatch: one fence per batch
-                if ((i + 1) % kMgPubBatch == 0 || i + 1 == my_nchunks) {
-                    const long long w1 = clock64();
+        // Two independent streams, polled (never a blocking wait on one while
+        // the other is ready):
+        //  - produced chunks: once every producer warp arrived, one fence
+        //    (cumulative over their stores, acquired through the mbarrier),
+        //    then the chunk's flags (leaf flags of every produced rank, partial
+        //    flags). This depends on nothing but this CTA's producers, so
+        //    production is published whatever the peers do;
+        //  - owned reduced chunks (split plans): after the finishers' arrival,
+        //    one fence, then the reduced-chunk flags.
+        // No producer or finisher ever waits on a fence.
+        int64_t i = 0, x1 = 0, nown = 0;
+        int rmode = 0;  // reduce stream: 0 waiting for lock-in, 1 active, 2 done / none
+        uint64_t t0 = globaltimer();
+        int spins = 0;
+        while (i < my_nchunks || rmode < 2) {
+            bool prog = false;
+            // every produced chunk whose producers all arrived: one fence for the run
+            int64_t i1 = i;
+            if (lane == 0)
+                while (i1 < my_nchunks && i1 - i < kMgPub / 2 &&
+                       mbar_test_wait(&pd[int(i1 % kMgPub)], unsigned((i1 / kMgPub) & 1)))
+                    ++i1;
+            i1 = __shfl_sync(0xffffffffu, i1, 0);
+            if (i1 > i) {
+                prog = true;
+                const long long w1 = clock64();
+                if (lane == 0) fence_pub();
+                __syncwarp();
+                if (lane == 0 && p.prof) prof_add(9, clock64() - w1);
+                for (int64_t b = i; b < i1; ++b) {
+                    const int64_t tb = c_of(b) * kLocTiles;
+                    const int nt = int(p.n_tiles - tb < kLocTiles ? p.n_tiles - tb : kLocTiles);
+                    for (int e = lane; e < J * nt * kWarps; e += 32) {
+                        const int w = e % kWarps, tt = (e / kWarps) % nt, j = e / (kWarps * nt);
+                        const DevJob& jb = p.jobs[j];
+                        if (jb.produces) st_relaxed_sys(flag_ptr(p, jb.rank, tb + tt, w), jb.version);
+                    }
+                    for (int e = lane; e < p.n_parts * nt; e += 32)
+                        st_relaxed_sys(s_pflag[e / nt] + tb + e % nt, p.part_version[e / nt]);
+                }
+                __syncwarp();
+                if (lane == 0)
+                    for (int64_t b = i; b < i1; ++b) mbar_arrive(&pk[int(b % kMgPub)]);
+                i = i1;
+            }
+            if (rmode == 0 && ready != 0) {
+                __threadfence_block();
+                rmode = ready == 1 ? 1 : 2;
+            }
+            if (rmode == 1) {
+                // owned reduced chunks the finishers handed over: one fence for the run
+                auto owned = [&](int64_t x) {
+                    bool o = false;
+                    for (int pl = 0; pl < NP; ++pl) o = o || (s_mode[pl] == kMgSplit && ph1(pl, x));
+                    return o;
+                };
+                while (x1 < my_nchunks && !owned(x1)) ++x1;
+                int64_t n1 = nown, y = x1;
+                if (lane == 0)
+                    while (y < my_nchunks && n1 - nown < kMgPub / 2 &&
+                           mbar_test_wait(&rd[int(n1 % kMgPub)], unsigned((n1 / kMgPub) & 1))) {
+                        ++n1;
+                        ++y;
+                        while (y < my_nchunks && !owned(y)) ++y;
+                    }
+                n1 = __shfl_sync(0xffffffffu, n1, 0);
+                if (n1 > nown) {
+                    prog = true;
                     if (lane == 0) fence_pub();
                     __syncwarp();
-                    if (lane == 0 && p.prof) {
-                        prof_add(8, w1 - w0);
-                        prof_add(9, clock64() - w1);
+                    for (int64_t k = nown; k < n1; ++k) {
+                        const int64_t tb = c_of(x1) * kLocTiles;
+                        const int nt = int(p.n_tiles - tb < kLocTiles ? p.n_tiles - tb : kLocTiles);
+                        for (int pl = 0; pl < NP; ++pl)
+                            if (s_mode[pl] == kMgSplit && ph1(pl, x1) && lane < nt)
+                                st_relaxed_sys(s_redflag[pl][owner(pl, x1)] + tb + lane, s_ver[pl]);
+                        ++x1;
+                        while (x1 < my_nchunks && !owned(x1)) ++x1;
                     }
-                    for (int64_t b = i - i % kMgPubBatch; b <= i; ++b) {
-                        const int64_t c = int64_t(blockIdx.x) + b * gridDim.x;
-                        const int64_t t0 = c * kLocTiles;
-                        const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
-                        for (int e = lane; e < J * nt * kWarps; e += 32) {
-                            const int w = e % kWarps, tt = (e / kWarps) % nt, j = e / (kWarps * nt);
-                            const DevJob& jb = p.jobs[j];
-                            if (jb.produces) st_relaxed_sys(flag_ptr(p, jb.rank, t0 + tt, w), jb.version);
-                        }
-                        for (int e = lane; e < p.n_parts * nt; e += 32)
-                            st_relaxed_sys(s_pflag[e / nt] + t0 + e % nt, p.part_version[e / nt]);
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&pk[int(b % kMgPub)]);
-                    }
-                } else if (lane == 0 && p.prof) {
-                    prof_add(8, clock64() - w0);
+                    __syncwarp();
+                    if (lane == 0)
+                        for (int64_t k = nown; k < n1; ++k) mbar_arrive(&rk[int(k % kMgPub)]);
+                    nown = n1;
                 }
+                if (x1 >= my_nchunks) rmode = 2;
             }
-            const int64_t x1 = i - kMgLag1;
-            if (x1 < 0 || x1 >= my_nchunks) continue;
-            if (x1 == 0) {
-                while (ready == 0) __nanosleep(64);
-                __threadfence_block();
-                res = ready == 1;
-                if (!res) break;
+            if (prog) {
+                spins = 0;
+                t0 = globaltimer();
+            } else {
+                __nanosleep(32);
+                if ((++spins & 255) == 0 && (globaltimer() - t0 > uint64_t(p.timeout_ns) || aborted(p)))
+                    break;  // the waiting side reports the timeout
             }
-            bool owned = false;
-            for (int pl = 0; pl < NP; ++pl) owned = owned || (s_mode[pl] == kMgSplit && s_ownlocal[pl][owner(pl, x1)]);
-            if (!owned) continue;
-            const int slot = int(nown % kMgPub);
-            if (!mbar_wait(p, &rd[slot], unsigned((nown / kMgPub) & 1))) break;
-            if (lane == 0) fence_pub();
-            __syncwarp();
-            const int64_t c = int64_t(blockIdx.x) + x1 * gridDim.x;
-            const int64_t t0 = c * kLocTiles;
-            const int nt = int(p.n_tiles - t0 < kLocTiles ? p.n_tiles - t0 : kLocTiles);
-            for (int pl = 0; pl < NP; ++pl)
-                if (s_mode[pl] == kMgSplit && s_ownlocal[pl][owner(pl, x1)] && lane < nt)
-                    st_relaxed_sys(s_redflag[pl][owner(pl, x1)] + t0 + lane, s_ver[pl]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&rk[slot]);
-            ++nown;
         }
         if (lane == 0) prof_add(10, clock64() - kt0);
-    } else if (warp < 4 + kMgProd / 32) {
+    } else if (warp < kMgRoleWarps + kMgProd / 32) {
         // ---------------- producers: W', partials ----------------
         // Free-running: they never wait on another GPU, only on the input
-        // ring and (8 chunks back) on the publisher.
+        // ring and (kMgPub chunks back) on the produce publisher.
         constexpr int VP = C / kMgProd;
-        const int ct = tid - 128;
+        const int ct = tid - kMgRoleWarps * 32;
         unsigned bad = 0;
         int sti = 0;
         unsigned phi = 0;
         bool ok = true;
         for (int64_t i = 0; ok && i < my_nchunks; ++i) {
-            const int64_t c = int64_t(blockIdx.x) + i * gridDim.x;
-            const int64_t e0 = c * chunk_elems;
+            const int64_t e0 = c_of(i) * chunk_elems;
             const bool fullc = e0 + chunk_elems <= p.n;
             for (int jj = 0; jj < J; ++jj) {
                 const int j = p.job_order[jj];
@@ -2291,7 +2307,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
     } else {
         // ---------------- finishers: phase 1 and phase 2 ----------------
         constexpr int VF = C / kMgFin;
-        const int ct = tid - 128 - kMgProd;
+        const int ct = tid - kMgRoleWarps * 32 - kMgProd;
         int sta = 0, stb = 0;
         unsigned pha = 0, phb = 0;
         int64_t nown = 0;  // owned reduced chunks handed to the publisher
@@ -2305,92 +2321,82 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
         constexpr int kLagB = kMgLag2 - kMgLag1;  // phase 2 trails phase 1 by this many chunks
         for (int64_t i = 0; ready == 1 && ok && i < my_nchunks + kLagB; ++i) {
             const int64_t x1 = i;
-            if (x1 < my_nchunks) {
+            if (x1 < my_nchunks && rows_a_of(x1) >= 0) {
                 // ---- phase 1 of chunk x1 ----
-                const int64_t c = int64_t(blockIdx.x) + x1 * gridDim.x;
-                const int64_t e0 = c * chunk_elems;
-                int ra, rb;
-                rows_of(x1, ra, rb);
-                if (ra) {
-                    const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
-                    if (!mbar_wait(p, &fa[sta], pha)) {
+                const int64_t e0 = c_of(x1) * chunk_elems;
+                const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
+                if (!mbar_wait(p, &fa[sta], pha)) {
+                    ok = false;
+                    break;
+                }
+                if (p.prof && ct == 0) prof_add(2, clock64() - w0);
+                const V* lb = rows_a + size_t(sta) * s_rows_a * C;
+                bool owned = false;
+                int e = 0;
+                for (int pl = 0; pl < NP; ++pl) {
+                    if (!ph1(pl, x1)) continue;
+                    const DevPlan& P_ = p.plans[pl];
+#pragma unroll
+                    for (int kv = 0; kv < VF; ++kv) {
+                        const int v = kv * kMgFin + ct;
+                        const int64_t idx = e0 + int64_t(v) * E;
+                        if (idx >= p.npad) continue;
+                        auto fetch = [&](int leaf) -> V {
+                            const int row = s_erow[pl][leaf];
+                            if (row >= 0) return lb[(e + row) * C + v];
+                            return __ldcg(reinterpret_cast<const V*>(s_esrc[pl][leaf] + idx));
+                        };
+                        const V acc = tree_sum<T>(fetch, s_elog[pl]);
+                        if (s_mode[pl] == kMgSplit)  // the owner's reduced chunk, for the other members
+                            __stcg(reinterpret_cast<V*>(s_red[pl][owner(pl, x1)] + idx), acc);
+                        finish_members<T>(p, sm, P_, acc, idx, [&](int j) {
+                            return __ldcg(reinterpret_cast<const V*>(s_job[j].ring + idx));
+                        });
+                    }
+                    owned = owned || s_mode[pl] == kMgSplit;
+                    e += s_nrow[pl];
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ea[sta]);
+                if (++sta == s_nsa) sta = 0, pha ^= 1u;
+                if (owned) {  // the reduced chunk to the reduce publisher
+                    const int slot = int(nown % kMgPub);
+                    if (nown >= kMgPub && !mbar_wait(p, &rk[slot], unsigned(((nown / kMgPub) - 1) & 1))) {
                         ok = false;
                         break;
                     }
-                    if (p.prof && ct == 0) prof_add(2, clock64() - w0);
-                    const V* lb = rows_a + size_t(sta) * s_rows_a * C;
-                    bool owned = false;
-                    int e = 0;
-                    for (int pl = 0; pl < NP; ++pl) {
-                        if (s_mode[pl] == kMgSplit && !s_ownlocal[pl][owner(pl, x1)]) continue;
-                        const DevPlan& P_ = p.plans[pl];
-#pragma unroll
-                        for (int kv = 0; kv < VF; ++kv) {
-                            const int v = kv * kMgFin + ct;
-                            const int64_t idx = e0 + int64_t(v) * E;
-                            if (idx >= p.npad) continue;
-                            auto fetch = [&](int leaf) -> V {
-                                const int row = s_erow[pl][leaf];
-                                if (row >= 0) return lb[(e + row) * C + v];
-                                return __ldcg(reinterpret_cast<const V*>(s_esrc[pl][leaf] + idx));
-                            };
-                            const V acc = tree_sum<T>(fetch, s_elog[pl]);
-                            if (s_mode[pl] == kMgSplit)  // the owner's reduced chunk, for the other members
-                                __stcg(reinterpret_cast<V*>(s_red[pl][owner(pl, x1)] + idx), acc);
-                            finish_members<T>(p, sm, P_, acc, idx, [&](int j) {
-                                return __ldcg(reinterpret_cast<const V*>(s_job[j].ring + idx));
-                            });
-                        }
-                        owned = owned || s_mode[pl] == kMgSplit;
-                        e += s_nrow[pl];
-                    }
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&ea[sta]);
-                    if (++sta == s_nsa) sta = 0, pha ^= 1u;
-                    if (owned) {  // the reduced chunk to the publisher
-                        const int slot = int(nown % kMgPub);
-                        if (nown >= kMgPub && !mbar_wait(p, &rk[slot], unsigned(((nown / kMgPub) - 1) & 1))) {
-                            ok = false;
-                            break;
-                        }
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&rd[slot]);
-                        ++nown;
-                    }
+                    if (lane == 0) mbar_arrive(&rd[slot]);
+                    ++nown;
                 }
             }
             const int64_t x2 = i - kLagB;
-            if (x2 >= 0 && x2 < my_nchunks) {
+            if (x2 >= 0 && x2 < my_nchunks && rows_b_of(x2) >= 0) {
                 // ---- phase 2 of chunk x2: reduced chunks owned elsewhere ----
-                const int64_t c = int64_t(blockIdx.x) + x2 * gridDim.x;
-                const int64_t e0 = c * chunk_elems;
-                int ra, rb;
-                rows_of(x2, ra, rb);
-                if (rb) {
-                    if (!mbar_wait(p, &fb[stb], phb)) {
-                        ok = false;
-                        break;
-                    }
-                    const V* lb = rows_b + size_t(stb) * s_rows_b * C;
-                    int e = 0;
-                    for (int pl = 0; pl < NP; ++pl) {
-                        if (s_mode[pl] != kMgSplit || s_ownlocal[pl][owner(pl, x2)]) continue;
-                        const DevPlan& P_ = p.plans[pl];
-#pragma unroll
-                        for (int kv = 0; kv < VF; ++kv) {
-                            const int v = kv * kMgFin + ct;
-                            const int64_t idx = e0 + int64_t(v) * E;
-                            if (idx >= p.npad) continue;
-                            finish_members<T>(p, sm, P_, lb[e * C + v], idx, [&](int j) {
-                                return __ldcg(reinterpret_cast<const V*>(s_job[j].ring + idx));
-                            });
-                        }
-                        ++e;
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&eb[stb]);
-                    if (++stb == s_nsb) stb = 0, phb ^= 1u;
+                const int64_t e0 = c_of(x2) * chunk_elems;
+                if (!mbar_wait(p, &fb[stb], phb)) {
+                    ok = false;
+                    break;
                 }
+                const V* lb = rows_b + size_t(stb) * s_rows_b * C;
+                int e = 0;
+                for (int pl = 0; pl < NP; ++pl) {
+                    if (ph1(pl, x2)) continue;
+                    const DevPlan& P_ = p.plans[pl];
+#pragma unroll
+                    for (int kv = 0; kv < VF; ++kv) {
+                        const int v = kv * kMgFin + ct;
+                        const int64_t idx = e0 + int64_t(v) * E;
+                        if (idx >= p.npad) continue;
+                        finish_members<T>(p, sm, P_, lb[e * C + v], idx, [&](int j) {
+                            return __ldcg(reinterpret_cast<const V*>(s_job[j].ring + idx));
+                        });
+                    }
+                    ++e;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&eb[stb]);
+                if (++stb == s_nsb) stb = 0, phb ^= 1u;
             }
         }
         if (!ok) {
@@ -2408,6 +2414,8 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
     if (blockIdx.x == 0) {
         __syncthreads();
         const bool res = ready == 1;
+        if (res && threadIdx.x < 32) check_sync_points(p, sm);
+        __syncthreads();
         if (tid < p.n_jobs) {
             const DevJob& jb = p.jobs[tid];
             wg_job_status stt;
@@ -2818,6 +2826,8 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     if (blockIdx.x == 0) {
         __syncthreads();
         const bool res = ready == 1;
+        if (res && threadIdx.x < 32) check_sync_points(p, sm);
+        __syncthreads();
         if (tid < p.n_jobs) {
             const DevJob& jb = p.jobs[tid];
             wg_job_status stt;
@@ -3482,6 +3492,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     if (blockIdx.x == 0) {
         __syncthreads();
         const bool res = ready == 1;
+        if (res && threadIdx.x < 32) check_sync_points(p, sm);
+        __syncthreads();
         if (tid < p.n_jobs) {
             const DevJob& jb = p.jobs[tid];
             wg_job_status stt;
@@ -3616,6 +3628,7 @@ struct wg_ctx {
     int use_loc;              // single-GPU launches: TMA kernel (else the cp.async kernel)
     int use_hier;             // multi-GPU: exchange GPU-local subtree partials where the tree allows
     int use_mg;               // hierarchical launches: the TMA-produce multi-GPU kernel (else the pull kernel)
+    int mg_nsi_max;           // wagma_mg_kernel: deepest input ring tried (WG_MG_NSI_MAX)
     int mg_dyn_max[2];        // dynamic shared memory available to wagma_mg_kernel<T>
     int adaptive_grace;       // activator skips the grace wait for ranks late at the previous version
     int loc_dyn_max[2];       // dynamic shared memory available to wagma_local_kernel<T>
@@ -3636,6 +3649,7 @@ const char* wg_strerror(int code) {
         case WG_ECUDA: return "CUDA runtime error";
         case WG_ENOMEM: return "out of memory";
         case WG_EDIVERGE: return "non-finite gradient or replica (divergence)";
+        case WG_ESYNC: return "mismatched sync points";
         default: return "unknown error";
     }
 }
@@ -3678,6 +3692,8 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     if (const char* hh = getenv("WG_HIER")) ctx->use_hier = atoi(hh);
     ctx->use_mg = 1;
     if (const char* mg = getenv("WG_MG")) ctx->use_mg = atoi(mg);
+    ctx->mg_nsi_max = WG_MG_IN_STAGES_MAX;
+    if (const char* ns = getenv("WG_MG_NSI_MAX")) ctx->mg_nsi_max = std::max(2, atoi(ns));
     ctx->adaptive_grace = 1;
     if (const char* ag = getenv("WG_ADAPTIVE_GRACE")) ctx->adaptive_grace = atoi(ag);
     ctx->fence_scope = 1;  // GPU scope for per-tile flags (see publish_tile)
@@ -3705,6 +3721,8 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     off = align_up(off + int64_t(ctx->R) * ctx->D * 8, 256);
     L.counter = off;
     off = align_up(off + int64_t(ctx->R) * ctx->D * 4, 256);
+    L.syncmark = off;
+    off = align_up(off + int64_t(ctx->R) * ctx->D * 8, 256);
     L.desc = off;
     off = align_up(off + int64_t(ctx->Dv) * int64_t(sizeof(Desc)), 256);
     L.flags = off;
@@ -3928,6 +3946,8 @@ int wg_install(wg_ctx* ctx, int rank, int64_t stamp, const void* vec, void* stre
     fill_i64_kernel<<<64, 256, 0, s>>>(flags, ctx->n_tiles * kWarps, stamp);
     int64_t* comp = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.complete) + int64_t(l) * ctx->D + slot;
     fill_i64_kernel<<<1, 32, 0, s>>>(comp, 1, stamp);
+    int64_t* mark = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.syncmark) + int64_t(l) * ctx->D + slot;
+    fill_i64_kernel<<<1, 32, 0, s>>>(mark, 1, 2 * (stamp + 1));
     int64_t* ann = reinterpret_cast<int64_t*>(ctx->arena + ctx->L.announce) + int64_t(l) * kAnnounceStride;
     fill_i64_kernel<<<1, 32, 0, s>>>(ann, 1, stamp);
     WG_CUDA(cudaGetLastError());
@@ -4073,7 +4093,9 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
                 dv.mode = dv.forced_idx >= 0 ? kForced : (c.activation_enabled ? kLive : kBlocking);
             }
         } else if ((p.versions[vi].mode == kSync) != sync) {
-            return fail(WG_EINVAL, "version %lld mixes sync and group jobs", (long long)in.version);
+            // collective.py:381-386: one rank syncs at t while another joins t as a group round
+            return fail(WG_ESYNC, "version %lld mixes sync and group jobs (mismatched sync points)",
+                        (long long)in.version);
         }
         d.vidx = vi;
     }
@@ -4281,27 +4303,42 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         wide = wide || (__builtin_popcount(gpus) >= ctx->split_span && p.owners[k].n == p.plans[k].n_leaves &&
                         split_pays(p.owners[k].n, __builtin_popcount(gpus)));
     }
-    int mg_rows_in = 0, mg_cap_a = 0, mg_cap_b = 0;
+    int mg_rows_in = 0, mg_cap_a = 0, mg_cap_b = 0, mg_nsi = 0;
     if (any_hier && ctx->use_mg) {
-        // wagma_mg_kernel: input ring + W' stage + phase-1 rows (at least one
-        // chunk of every plan's leaves: the pull fallback) + phase-2 rows
+        // wagma_mg_kernel shared memory, in chunk rows: input ring (3 rows per
+        // stage) + W' stage (one row per job) + phase-1 rows + phase-2 rows.
+        // Phase 1 must fit two chunks of the pull fallback (every remote leaf
+        // of every plan: a member may turn out stale at lock-in) and two of
+        // the hierarchical rows; phase 2 two chunks of reduced rows. The
+        // deepest input ring that leaves that much wins (bytes in flight per
+        // SM are what the produce stream is bound by).
         const int64_t row = int64_t(kLocChunkVecs) * 16;
         const int total_rows = int(ctx->mg_dyn_max[c.dtype == WG_F32 ? 0 : 1] / row);
-        mg_rows_in = WG_MG_IN_STAGES * 3 + n_jobs;
-        int n_split = 0;
+        int n_split = 0, n_remote = 0, hier_rows = 0;
         for (int k = 0; k < p.n_plans; ++k) {
+            for (int li = 0; li < p.plans[k].n_leaves; ++li) n_remote += p.plans[k].leaves[li] / ctx->R != c.gpu_index;
             if (!p.plan_hl[k]) continue;
             const int np = p.plans[k].n_leaves >> p.plan_hl[k];
             unsigned gpus = 0;
             for (int li = 0; li < p.plans[k].n_leaves; ++li) gpus |= 1u << (p.plans[k].leaves[li] / ctx->R);
             n_split += ctx->use_split && L_has_red(ctx) && split_pays(np, __builtin_popcount(gpus));
+            hier_rows += np - 1;  // the other GPUs' partials (this GPU's are read from L2)
         }
-        mg_cap_b = std::min(4 * n_split, std::max(0, (total_rows - mg_rows_in) / 3));
-        mg_cap_a = total_rows - mg_rows_in - mg_cap_b;
-        if (mg_cap_a < n_leaves_total || (n_split && mg_cap_b < n_split)) mg_cap_a = 0;  // does not fit
+        for (int nsi = std::min(ctx->mg_nsi_max, kLocMaxStages); nsi >= 2 && !mg_nsi; --nsi) {
+            const int rows_in = nsi * 3 + n_jobs;
+            const int rest = total_rows - rows_in;
+            const int cap_b = n_split ? std::min(8 * n_split, rest / 3) : 0;
+            const int cap_a = rest - cap_b;
+            if (cap_a >= std::max(n_remote, 2 * hier_rows) && cap_b >= 2 * n_split) {
+                mg_nsi = nsi;
+                mg_rows_in = rows_in;
+                mg_cap_a = cap_a;
+                mg_cap_b = cap_b;
+            }
+        }
     }
     if (mg_cap_a > 0) {
-        p.loc_stages = WG_MG_IN_STAGES;
+        p.loc_stages = mg_nsi;
         p.mg_cap_a = mg_cap_a;
         p.mg_cap_b = mg_cap_b;
         p.mg_split = ctx->use_split && L_has_red(ctx);

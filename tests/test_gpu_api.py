@@ -193,3 +193,22 @@ def test_activation_tree_message_counts(cuda):
     with pytest.raises(ProtocolFault):
         groups[0].handle_message(1, b"")
     ctx.close()
+
+
+def test_mismatched_sync_points_protocol_fault(cuda):
+    """collective.py:381-386: one rank joins iteration t as a global sync while
+    another joins t as a group round -> ProtocolFault (mismatched sync points),
+    not a hang. Co-located ranks share one launch, so the device rejects the
+    mixed launch (WG_ESYNC); across GPUs the kernels compare the sync marks
+    (test_gpu_multi.py::test_multigpu_mismatched_sync_points)."""
+    P = 2
+    ctx = DeviceContext(P, 2, 8, dtype=torch.float64, timeout_s=5.0)
+    got = {}
+    sync = SyncAllreduce(ctx, 0, P, on_complete=lambda t, tot: got.setdefault(t, tot))
+    node = Node(ctx, 1, P, 2, np.zeros(8))
+    with pytest.raises(ProtocolFault, match="mismatched sync points"):
+        with ctx.batch():
+            sync.join(3, np.ones(8))
+            node.group.join_or_check(3, np.ones(8))
+    assert not got
+    ctx.close()

@@ -155,3 +155,17 @@ def test_multigpu_baseline_size_bit_exact(tmp_path, hier, G, S):
     assert np.array_equal(Wdev, want)
     late = sum(int((stamps[v] >= -1).sum() - (stamps[v] == v).sum()) for v in range(T) if (v + 1) % tau)
     assert late > 0, "the injected straggler never contributed a stale model"
+
+
+def test_multigpu_mismatched_sync_points():
+    """collective.py:381-386 on the device: rank 0 (GPU 0) joins iteration 0 as
+    a global sync, rank 1 (GPU 1) as a group round; both GPUs latch WG_ESYNC
+    (ProtocolFault) instead of a watchdog timeout."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+            "--master-addr", "127.0.0.1", "--master-port", "29391",
+            os.path.join(ROOT, "tests", "sync_mismatch_worker.py")]
+    res = subprocess.run(args, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert "rank0 code=9" in res.stdout and "rank1 code=9" in res.stdout
