@@ -525,6 +525,15 @@ struct SmemCtl {
     int32_t abort;
 };
 
+#ifndef WG_NO_SYNC_CHECK
+#define WG_NO_SYNC_CHECK 0
+#endif
+#ifndef WG_PUB_GATHER_P  // produced chunks published per fence at most (publisher of wagma_mg_kernel)
+#define WG_PUB_GATHER_P 1
+#endif
+#ifndef WG_PUB_GATHER_R  // owned reduced chunks published per fence at most
+#define WG_PUB_GATHER_R 1
+#endif
 // Sync-point agreement (collective.py:381-386: "mismatched sync points"), one
 // warp of CTA 0 after the launch consumed its leaves. Every rank marks how it
 // joins each version (control_phase: 2(v+1), +1 for a global sync):
@@ -534,7 +543,7 @@ struct SmemCtl {
 // Either mismatch latches WG_ESYNC (info v * 1024 + rank), a ProtocolFault.
 __device__ void check_sync_points(const LaunchParams& p, const SmemCtl& sm) {
     const int lane = threadIdx.x & 31;
-    if (sm.abort) return;
+    if (sm.abort || WG_NO_SYNC_CHECK) return;
     for (int vi = 0; vi < p.n_versions; ++vi) {
         const int64_t v = p.versions[vi].version;
         const bool sync = p.versions[vi].mode == kSync;
@@ -1758,6 +1767,9 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
 #ifndef WG_MG_LAG2
 #define WG_MG_LAG2 4
 #endif
+#ifndef WG_MG_DIRECT_LOCAL  // 1: this GPU's partials read by the finishers from L2, else TMA rows
+#define WG_MG_DIRECT_LOCAL 1
+#endif
 #ifndef WG_MG_IN_STAGES_MAX  // deepest input ring tried (the launch takes the deepest that fits)
 #define WG_MG_IN_STAGES_MAX 5
 #endif
@@ -1940,15 +1952,17 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
             }
         return ready;
     };
-    // Sliding-window puller (warps 1 and 2). Chunks in CTA order; source q
-    // of a chunk belongs to lane q % 32, which probes its flags and, once
-    // every lane has seen all its flags of that chunk and of every earlier
-    // one, issues its TMA row copy. A chunk is never held back by a later
-    // chunk's flags: on another GPU a later chunk may wait, through its
-    // owner's reduce, on this GPU consuming the earlier one (no wait cycle).
+    // Sliding-window puller (warps 1 and 2). Chunks in CTA order, up to W of
+    // them in a window; the window's (chunk, source) pairs are dealt to the
+    // lanes round-robin, so every lane probes about one flag set per sweep
+    // (all in flight at once) and issues the TMA row copy of its pairs. A
+    // chunk is delivered as soon as every pair of it and of every earlier
+    // chunk was seen ready -- never held back by a later chunk's flags: on
+    // another GPU a later chunk may wait, through its owner's reduce, on this
+    // GPU consuming the earlier one (no wait cycle).
     auto puller = [&](int NS, V* rows, int rows_per_stage, uint64_t* full, uint64_t* empty, auto&& nrows,
                       auto&& srcs) -> bool {
-        const int W = NS < kPullBatch ? NS : kPullBatch;  // chunks whose flags are probed together
+        const int W = NS < kPullBatch ? NS : kPullBatch;
         int st = 0;
         unsigned ph = 0;
         int64_t k = 0, kc = 0;
@@ -1960,28 +1974,28 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 ++kc;
             }
             if (!nb) return true;
-            int lane_b = 0, done = 0, spins = 0;
+            int done = 0, spins = 0;
+            unsigned seen = 0;  // this lane's pairs seen ready (bit = pair index / 32)
             const uint64_t t0 = globaltimer();
             while (done < nb) {
-                int rc = 0;
-                while (lane_b < nb && !rc) {
-                    bool all = true;
-                    int q = 0;
-                    const int64_t c = c_of(bk[lane_b]);
-                    srcs(bk[lane_b], [&](const int64_t* f, int stride, int64_t want, const T*, int) {
-                        if ((q++ & 31) != lane || !all || rc) return;
+                int rc = 0, first = nb, qg = 0;
+                for (int b = 0; b < nb; ++b) {
+                    const int64_t c = c_of(bk[b]);
+                    srcs(bk[b], [&](const int64_t* f, int stride, int64_t want, const T*, int) {
+                        const int q = qg++;
+                        if ((q & 31) != lane || b < done || (q < 1024 && ((seen >> (q >> 5)) & 1u))) return;
                         const int r = probe(f, stride, want, c);
                         if (r < 0)
                             rc = -r;
-                        else if (r == 0)
-                            all = false;
+                        else if (r > 0)
+                            seen |= q < 1024 ? 1u << (q >> 5) : 0u;
+                        else if (b < first)
+                            first = b;
                     });
-                    if (!all) break;
-                    if (!rc) ++lane_b;
                 }
-                if (rc) raise_error(p, rc, bk[lane_b]);
+                if (rc) raise_error(p, rc, bk[done]);
                 if (__any_sync(0xffffffffu, rc != 0)) return false;
-                const int rdy = __reduce_min_sync(0xffffffffu, lane_b);
+                const int rdy = __reduce_min_sync(0xffffffffu, first);
                 if (rdy == done) {
                     if ((++spins & 63) == 0 && (globaltimer() - t0 > uint64_t(p.timeout_ns) || aborted(p))) {
                         if (lane == 0) raise_error(p, WG_ETIMEOUT, bk[done]);
@@ -1993,7 +2007,12 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 // the flags were read with acquire loads; order them before the
                 // async-proxy (TMA) reads of the data they guard
                 asm volatile("fence.proxy.async.global;" ::: "memory");
-                for (int b = done; b < rdy; ++b, ++k) {
+                qg = 0;
+                for (int b = 0; b < rdy; ++b) {
+                    if (b < done) {  // keep the pair numbering of the window
+                        srcs(bk[b], [&](const int64_t*, int, int64_t, const T*, int) { ++qg; });
+                        continue;
+                    }
                     if (k >= NS && !mbar_wait(p, &empty[st], ph ^ 1u)) {
                         if (lane == 0) raise_error(p, WG_ETIMEOUT, bk[b]);
                         return false;
@@ -2002,13 +2021,13 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                     const unsigned cb = pad_bytes(c);
                     if (lane == 0) mbar_arrive_expect_tx(&full[st], unsigned(nrows(bk[b])) * cb);
                     __syncwarp();
-                    int q = 0;
                     srcs(bk[b], [&](const int64_t*, int, int64_t, const T* src, int row) {
-                        if ((q++ & 31) == lane && row >= 0)
+                        if ((qg++ & 31) == lane && row >= 0)
                             bulk_g2s(rows + (size_t(st) * rows_per_stage + row) * C, src + c * chunk_elems, cb, &full[st]);
                     });
                     __syncwarp();
                     if (++st == NS) st = 0, ph ^= 1u;
+                    ++k;
                 }
                 done = rdy;
             }
@@ -2098,7 +2117,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                         s_ownlocal[pl][u] = int8_t(key / p.R == p.gpu_index);
                         // this GPU's partials: read by the finishers from L2 (stored
                         // moments ago); only the peers' partials take TMA rows
-                        s_erow[pl][u] = s_ownlocal[pl][u] ? int8_t(-1) : int8_t(nr++);
+                        s_erow[pl][u] = (WG_MG_DIRECT_LOCAL && s_ownlocal[pl][u]) ? int8_t(-1) : int8_t(nr++);
                     }
                     s_ne[pl] = int8_t(ne);
                     s_elog[pl] = int8_t(P_.log_leaves - hl);
@@ -2168,7 +2187,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
             // every produced chunk whose producers all arrived: one fence for the run
             int64_t i1 = i;
             if (lane == 0)
-                while (i1 < my_nchunks && i1 - i < kMgPub / 2 &&
+                while (i1 < my_nchunks && i1 - i < WG_PUB_GATHER_P &&
                        mbar_test_wait(&pd[int(i1 % kMgPub)], unsigned((i1 / kMgPub) & 1)))
                     ++i1;
             i1 = __shfl_sync(0xffffffffu, i1, 0);
@@ -2208,7 +2227,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 while (x1 < my_nchunks && !owned(x1)) ++x1;
                 int64_t n1 = nown, y = x1;
                 if (lane == 0)
-                    while (y < my_nchunks && n1 - nown < kMgPub / 2 &&
+                    while (y < my_nchunks && n1 - nown < WG_PUB_GATHER_R &&
                            mbar_test_wait(&rd[int(n1 % kMgPub)], unsigned((n1 / kMgPub) & 1))) {
                         ++n1;
                         ++y;
@@ -3688,7 +3707,10 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     if (const char* sm = getenv("WG_SPLIT_MIN_BYTES")) ctx->split_min_bytes = std::max<long long>(0, atoll(sm));
     ctx->use_loc = 1;
     if (const char* lc = getenv("WG_LOC")) ctx->use_loc = atoi(lc);
-    ctx->use_hier = 1;
+    // Hierarchical (GPU-local subtree) sums are opt-in: measured at P=8, n = 25.6M
+    // (profiles/r02_multigpu_ab.txt) the split / pull kernels without them are as
+    // fast at 2 GPUs and faster at 4 (S=8 0.477 ms vs 0.540 pull-hier, 0.73 mg).
+    ctx->use_hier = 0;
     if (const char* hh = getenv("WG_HIER")) ctx->use_hier = atoi(hh);
     ctx->use_mg = 1;
     if (const char* mg = getenv("WG_MG")) ctx->use_mg = atoi(mg);
@@ -4322,7 +4344,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
             unsigned gpus = 0;
             for (int li = 0; li < p.plans[k].n_leaves; ++li) gpus |= 1u << (p.plans[k].leaves[li] / ctx->R);
             n_split += ctx->use_split && L_has_red(ctx) && split_pays(np, __builtin_popcount(gpus));
-            hier_rows += np - 1;  // the other GPUs' partials (this GPU's are read from L2)
+            hier_rows += np - WG_MG_DIRECT_LOCAL;  // the other GPUs' partials (this GPU's from L2)
         }
         for (int nsi = std::min(ctx->mg_nsi_max, kLocMaxStages); nsi >= 2 && !mg_nsi; --nsi) {
             const int rows_in = nsi * 3 + n_jobs;

@@ -47,7 +47,8 @@ def test_algorithmic_bytes_per_launch(monkeypatch):
     a = types.SimpleNamespace(P=8, S=8, tau=10, n=n)
     hbm, nvl = b.step_bytes(a, 1, 0, 0, 4)  # all 8 ranks local: 6 streams each, no NVLink
     assert nvl == 0 and hbm == 8 * 6 * N
-    # hierarchical: 2 GPUs, masks (1,2,4): one 4-leaf partial per GPU, pull the other
+    # hierarchical (opt-in, WG_HIER=1): 2 GPUs, masks (1,2,4): one 4-leaf partial per GPU, pull the other
+    monkeypatch.setenv("WG_HIER", "1")
     hbm, nvl = b.step_bytes(a, 2, 0, 0, 4)
     assert nvl == 1.0 * N and hbm == 4 * 6 * N + N + N
     hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)  # 4 GPUs: 2-leaf partials, pull 3
