@@ -129,8 +129,39 @@ def _run(ctx: DeviceContext, items: list[_Pending]) -> None:
     except DeviceProtocolFault as exc:
         ctx.clear_error()
         raise _fault(exc) from exc
-    for it, st in zip(items, ctx.statuses()):
+    statuses = ctx.statuses()
+    for it, st in zip(items, statuses):
         it.resolve(st)
+    _passive_completions(ctx, items, statuses)
+
+
+def _passive_completions(ctx: DeviceContext, items: list[_Pending], statuses) -> None:
+    """Fire the passive completions of this process's endpoints that did not
+    join a version a group member just ran (wait-avoiding mode only): the
+    group's sum is the launched member's accumulator (every member of a group
+    gets the same bits), the stamp is the one the activation locked."""
+    eps = getattr(ctx, "_wg_endpoints", None)
+    if not eps or not ctx.activation_enabled:
+        return
+    from .topology import GroupingParams, compute_groups
+    launched: dict[int, dict[int, tuple[Job, object]]] = {}
+    for it, st in zip(items, statuses):
+        if it.job.kind == _lib.WG_JOB_GROUP_SUM and it.job.acc_out is not None:
+            launched.setdefault(it.job.version, {})[it.job.rank] = (it.job, st)
+    for v, jobs in launched.items():
+        waiting = [q for q, ep in eps.items()
+                   if q not in jobs and ep.last_joined < v and v not in ep.completed and v not in ep.execution_count]
+        if not waiting:
+            continue
+        stamps, locked = ctx.query_version(v)
+        if not locked:
+            continue
+        part = compute_groups(GroupingParams(ctx.P, ctx.S, v), ctx.mask_rule)
+        for q in waiting:
+            src = next((jobs[r] for r in part.group_of(q) if r in jobs), None)
+            if src is None or stamps[q] >= v:
+                continue
+            eps[q]._passive_complete(v, src[0].acc_out.clone(), int(stamps[q]), src[1].root)
 
 
 @contextmanager
@@ -211,6 +242,13 @@ class GroupAllreduce:
         self.acts_sent = 0
         self.phases_sent = 0
         self._group_phases = S.bit_length() - 1
+        # finished versions this rank took part in passively (stale buffer),
+        # handed back by its late join (collective.py:208, :341-343)
+        self.completed: dict[int, tuple[torch.Tensor, bool, int]] = {}
+        eps = getattr(ctx, "_wg_endpoints", None)
+        if eps is None:
+            eps = ctx._wg_endpoints = {}
+        eps[rank] = self
 
     def install_fresh(self, vec, iteration: int) -> None:
         self.send_buffer.install(vec, iteration)
@@ -222,6 +260,27 @@ class GroupAllreduce:
         """The reference's transport hook (collective.py:226-233). Device memory
         is the transport here: peers never exchange host messages."""
         raise ProtocolFault(f"rank {self.rank}: no host messages on the device transport (from {src})")
+
+    def _executed(self, version: int, stamp: int, root: int, activator: bool) -> None:
+        """Bookkeeping of one execution of `version` (collective.py:283-308, 319)."""
+        self.execution_count[version] = self.execution_count.get(version, 0) + 1
+        if activator:
+            self.activations_originated += 1
+        self.acts_sent += self._acts_for(root)
+        self.phases_sent += self._group_phases
+        if self.contribution_log is not None:
+            self.contribution_log.append((self.rank, version, stamp))
+
+    def _passive_complete(self, version: int, acc: torch.Tensor, stamp: int, root: int) -> None:
+        """Passive participation (collective.py:138-141, 331-345): a group member
+        activated `version` while this rank had not joined; its stale send
+        buffer (stamp < version) was summed, and the finished accumulator is
+        delivered here, not timely, before this rank's own join."""
+        self._executed(version, stamp, root, False)
+        self.last_completed = max(self.last_completed, version)
+        self.completion_tag = version
+        self.completed[version] = (acc, False, stamp)
+        self.on_complete(version, acc, False, stamp)
 
     def join_or_check(self, version: int, fresh) -> JoinResult:
         """Join version ``version`` with the fresh local model (collective.py:192-222)."""
@@ -238,15 +297,16 @@ class GroupAllreduce:
 
         def resolve(st):
             self.send_buffer.stamped_iteration = version
-            self.execution_count[version] = self.execution_count.get(version, 0) + 1
-            if st.activator:
-                self.activations_originated += 1
-            self.acts_sent += self._acts_for(st.root)
-            self.phases_sent += self._group_phases
-            if self.contribution_log is not None:
-                self.contribution_log.append((self.rank, version, st.contrib_stamp))
             self.last_completed = max(self.last_completed, version)
             self.completion_tag = version
+            if version in self.completed:
+                # it already took part passively (its stale buffer was locked in
+                # when a group member activated): the finished accumulator
+                # (collective.py:206-208); the device result is bit-identical
+                result.status = JoinStatus.ALREADY_DONE
+                result.accumulator = self.completed.pop(version)[0]
+                return
+            self._executed(version, st.contrib_stamp, st.root, st.activator)
             if st.timely:
                 self.on_complete(version, acc, True, st.contrib_stamp)
             else:

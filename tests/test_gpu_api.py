@@ -212,3 +212,32 @@ def test_mismatched_sync_points_protocol_fault(cuda):
             node.group.join_or_check(3, np.ones(8))
     assert not got
     ctx.close()
+
+
+def test_straggler_passive_completion_then_already_done(cuda):
+    """Restates test_collective.py:124-155 (reference): group {0,1} at version 0,
+    rank 1 slow. Rank 0 sums fresh_0 + stale_1; rank 1's endpoint completes
+    passively (on_complete, not timely, stamp -1) before its own join, which
+    returns ALREADY_DONE with the finished sum and installs its fresh model."""
+    P, S, d = 4, 2, 2
+    stale = [np.full(d, -float(r + 1)) for r in range(P)]
+    fresh = [np.arange(d, dtype=np.float64) + 10.0 * (r + 1) for r in range(P)]
+    ctx = DeviceContext(P, S, d, dtype=torch.float64, timeout_s=5.0)
+    nodes = [Node(ctx, r, P, S, stale[r]) for r in range(P)]
+    with ctx.batch():
+        for r in (0, 2, 3):
+            nodes[r].group.join_or_check(0, fresh[r])
+    acc0, timely0, _ = nodes[0].results[0]
+    assert np.array_equal(acc0, fresh[0] + stale[1]) and timely0
+    acc1, timely1, stamp1 = nodes[1].results[0]  # passive completion, before rank 1 joined
+    assert np.array_equal(acc1, fresh[0] + stale[1])
+    assert not timely1 and stamp1 == -1
+    assert nodes[1].group.execution_count[0] == 1
+    res = nodes[1].group.join_or_check(0, fresh[1])
+    assert res.status is JoinStatus.ALREADY_DONE
+    assert np.array_equal(res.accumulator.cpu().numpy(), fresh[0] + stale[1])
+    # fresh model stays in the send buffer for future pulls
+    assert np.array_equal(nodes[1].group.send_buffer.payload.cpu().numpy(), fresh[1])
+    assert nodes[1].group.send_buffer.stamped_iteration == 0
+    assert nodes[1].group.execution_count[0] == 1  # executed exactly once (A4)
+    ctx.close()
