@@ -1804,6 +1804,10 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
     __shared__ __align__(8) uint64_t fa[kMgMaxStagesA], ea[kMgMaxStagesA];       // phase-1 rows
     __shared__ __align__(8) uint64_t fb[kMgMaxStagesB], eb[kMgMaxStagesB];       // phase-2 rows
     __shared__ volatile int ready;
+    // chunks of this CTA whose W' (every job) and partials the producers have
+    // stored: the finishers read this launch's own W' (late members) and
+    // this GPU's sources straight from L2 only below this count
+    __shared__ volatile long long s_produced;
     __shared__ int s_nsa, s_nsb, s_rows_a, s_rows_b;
     // consumers -> publisher: chunk produced (pd) / owned chunk reduced (rd); acks (pk, rk)
     __shared__ __align__(8) uint64_t pd[kMgPub], pk[kMgPub], rd[kMgPub], rk[kMgPub];
@@ -1842,6 +1846,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
     if (tid == 0) {
         sm.abort = 0;
         ready = 0;
+        s_produced = 0;
         for (int st = 0; st < NSI; ++st) {
             mbar_init(&fin[st], 1);
             mbar_init(&ein[st], kMgProd / 32);
@@ -2193,6 +2198,10 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
             i1 = __shfl_sync(0xffffffffu, i1, 0);
             if (i1 > i) {
                 prog = true;
+                if (lane == 0) {  // the producers' stores (acquired through pd) before the count
+                    __threadfence_block();
+                    s_produced = i1;
+                }
                 const long long w1 = clock64();
                 if (lane == 0) fence_pub();
                 __syncwarp();
@@ -2344,6 +2353,22 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                 // ---- phase 1 of chunk x1 ----
                 const int64_t e0 = c_of(x1) * chunk_elems;
                 const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
+                // this CTA's producers are done with chunk x1 (a stale group's leaves
+                // may all be complete older slots: then no flag orders this launch's
+                // own W' -- read by late members -- before its use)
+                if (s_produced <= x1) {
+                    const uint64_t tw = globaltimer();
+                    int it = 0;
+                    while (s_produced <= x1) {
+                        if ((++it & 255) == 0 && (globaltimer() - tw > uint64_t(p.timeout_ns) || aborted(p))) {
+                            ok = false;
+                            break;
+                        }
+                        __nanosleep(32);
+                    }
+                    if (!ok) break;
+                }
+                __threadfence_block();
                 if (!mbar_wait(p, &fa[sta], pha)) {
                     ok = false;
                     break;
