@@ -169,3 +169,33 @@ def test_multigpu_mismatched_sync_points():
     res = subprocess.run(args, capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert "rank0 code=9" in res.stdout and "rank1 code=9" in res.stdout
+
+
+STRESS_CASES = [
+    # G, P, S, families: default kernels (split / pull, GPU-scope flag fences) and the hierarchical ones
+    (2, 8, 8), (4, 8, 8), (4, 8, 4), (4, 4, 2),
+]
+
+
+@pytest.mark.parametrize("G,P,S", STRESS_CASES)
+def test_multigpu_stress_pipelined_rounds(tmp_path, hier, G, P, S):
+    """Memory-model stress (the default GPU-scope flag fences rely
+    on peers' loads being served by the owner's L2): 300 pipelined iterations
+    (no host synchronisation between launches), a rotating straggler GPU,
+    ragged n of a few chunks so flag publication and consumption race on every
+    tile; every replica must stay bit-exact against the oracle."""
+    if _ngpus() < G:
+        pytest.skip(f"needs {G} GPUs")
+    T, tau, n = 300, 10, 3 * 2048 + 7
+    port = 29700 + (hash((G, P, S, hier["WG_HIER"], hier["WG_MG"])) % 200)
+    outs = _run(tmp_path, G, port, env_extra=hier, P=P, S=S, T=T, tau=tau, nelem=n, dtype="f32", victims=1,
+                pipelined=1, delay_us=40)
+    R = P // G
+    W = np.stack([outs[r // R][f"W{r}"] for r in range(P)])
+    grads = np.stack([np.stack([outs[r // R][f"g{t}_{r}"] for r in range(P)]) for t in range(T)])
+    stamps = outs[0]["stamps"]
+    want = wo.replay_training(P=P, S=S, tau=tau, T=T, w0=outs[0]["w0"], grads=grads, etas=np.full((T, P), 0.05),
+                              stamps=stamps, update_rule="momentum", momentum=0.9, dtype=np.float32)
+    assert np.array_equal(W, want)
+    late = sum(int((stamps[v] >= -1).sum() - (stamps[v] == v).sum()) for v in range(T) if (v + 1) % tau)
+    assert late > 0, "the rotating straggler never contributed a stale model"
