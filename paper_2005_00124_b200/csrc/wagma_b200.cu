@@ -1770,6 +1770,9 @@ __global__ void __launch_bounds__(kLocThreads, 1) wagma_local_kernel(const __gri
 #ifndef WG_MG_DIRECT_LOCAL  // 1: this GPU's partials read by the finishers from L2, else TMA rows
 #define WG_MG_DIRECT_LOCAL 1
 #endif
+#ifndef WG_MG_SELF_PUB  // 1: the last producer warp of a chunk publishes it (the publisher warp only reduced chunks)
+#define WG_MG_SELF_PUB 0
+#endif
 #ifndef WG_MG_IN_STAGES_MAX  // deepest input ring tried (the launch takes the deepest that fits)
 #define WG_MG_IN_STAGES_MAX 5
 #endif
@@ -1811,6 +1814,9 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
     __shared__ int s_nsa, s_nsb, s_rows_a, s_rows_b;
     // consumers -> publisher: chunk produced (pd) / owned chunk reduced (rd); acks (pk, rk)
     __shared__ __align__(8) uint64_t pd[kMgPub], pk[kMgPub], rd[kMgPub], rk[kMgPub];
+    // WG_MG_SELF_PUB: per-chunk arrival counters of the producer warps (the
+    // last warp to finish a chunk fences and raises its flags)
+    __shared__ unsigned s_pubcnt[kPubRing];
     // local partials: buffers, flags and their leaf jobs in leaf order
     __shared__ T* s_part[kMaxJobs];
     __shared__ int64_t* s_pflag[kMaxJobs];
@@ -1847,6 +1853,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
         sm.abort = 0;
         ready = 0;
         s_produced = 0;
+        for (int q = 0; q < kPubRing; ++q) s_pubcnt[q] = 0;
         for (int st = 0; st < NSI; ++st) {
             mbar_init(&fin[st], 1);
             mbar_init(&ein[st], kMgProd / 32);
@@ -2187,6 +2194,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
         int rmode = 0;  // reduce stream: 0 waiting for lock-in, 1 active, 2 done / none
         uint64_t t0 = globaltimer();
         int spins = 0;
+        if (WG_MG_SELF_PUB) i = my_nchunks;  // the producers publish their own chunks
         while (i < my_nchunks || rmode < 2) {
             bool prog = false;
             // every produced chunk whose producers all arrived: one fence for the run
@@ -2315,16 +2323,54 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
                     __stcg(reinterpret_cast<V*>(s_part[pid] + idx), tree_sum<T>(fetch, s_plog[pid]));
                 }
             }
-            // hand the chunk to the publisher (fence + flags off this path)
-            const int slot = int(i % kMgPub);
-            const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
-            if (i >= kMgPub && !mbar_wait(p, &pk[slot], unsigned(((i / kMgPub) - 1) & 1))) {
-                ok = false;
-                break;
+            if (WG_MG_SELF_PUB) {
+                // the last producer warp to finish chunk i issues one fence
+                // (cumulative over the other warps' stores, acquired through the
+                // shared-memory counter) and raises the chunk's flags; warps
+                // drift by at most the input ring, far less than kPubRing chunks
+                __syncwarp();
+                unsigned old = 0;
+                if (lane == 0) {
+                    unsigned* cnt = &s_pubcnt[i & (kPubRing - 1)];
+                    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                                 : "=r"(old)
+                                 : "r"(smem_u32(cnt))
+                                 : "memory");
+                    if (old == kMgProd / 32 - 1) *cnt = 0;
+                }
+                old = __shfl_sync(0xffffffffu, old, 0);
+                if (old == kMgProd / 32 - 1) {
+                    const long long w1 = clock64();
+                    if (lane == 0) fence_pub();
+                    __syncwarp();
+                    if (lane == 0 && p.prof) prof_add(9, clock64() - w1);
+                    const int64_t tb = c_of(i) * kLocTiles;
+                    const int nt = int(p.n_tiles - tb < kLocTiles ? p.n_tiles - tb : kLocTiles);
+                    for (int e = lane; e < J * nt * kWarps; e += 32) {
+                        const int w = e % kWarps, tt = (e / kWarps) % nt, j = e / (kWarps * nt);
+                        const DevJob& jb = p.jobs[j];
+                        if (jb.produces) st_relaxed_sys(flag_ptr(p, jb.rank, tb + tt, w), jb.version);
+                    }
+                    for (int e = lane; e < p.n_parts * nt; e += 32)
+                        st_relaxed_sys(s_pflag[e / nt] + tb + e % nt, p.part_version[e / nt]);
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence_block();
+                        if (s_produced < i + 1) s_produced = i + 1;
+                    }
+                }
+            } else {
+                // hand the chunk to the publisher (fence + flags off this path)
+                const int slot = int(i % kMgPub);
+                const long long w0 = (p.prof && ct == 0) ? clock64() : 0;
+                if (i >= kMgPub && !mbar_wait(p, &pk[slot], unsigned(((i / kMgPub) - 1) & 1))) {
+                    ok = false;
+                    break;
+                }
+                if (p.prof && ct == 0) prof_add(3, clock64() - w0);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pd[slot]);
             }
-            if (p.prof && ct == 0) prof_add(3, clock64() - w0);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&pd[slot]);
         }
         if (!ok) {
             if (lane == 0) raise_error(p, WG_ETIMEOUT, blockIdx.x);
