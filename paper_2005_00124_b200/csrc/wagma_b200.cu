@@ -2525,11 +2525,29 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
 // readiness flags published in chunks of kPubChunk by the last warp to
 // finish a chunk (one GPU-scope fence, cumulative over the other warps'
 // stores acquired through the shared-memory counter). Never waits on a peer.
+// A late member's own W' of this launch is read back from its send slot by
+// the consumer warps (finish_members' own_wp). When every leaf of its group
+// is a complete older slot or lives on another GPU, no polled flag orders
+// this CTA's producers' store of that tile before the read: wait until the
+// producers published the tile (CTA-local tile index kc).
+__device__ __forceinline__ void wait_produced(const LaunchParams& p, const volatile long long* produced, int64_t kc) {
+    if (*produced <= kc) {
+        const uint64_t t0 = globaltimer();
+        int it = 0;
+        while (*produced <= kc) {
+            if ((++it & 255) == 0 && (globaltimer() - t0 > uint64_t(p.timeout_ns) || aborted(p))) break;
+            __nanosleep(32);
+        }
+    }
+    __threadfence_block();
+}
+
 template <typename T, int kNvlDepth, bool HIER = false>
 __device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename Tr<T>::V* ring, int64_t my_ntiles,
                                                 unsigned* pub_count, T* const* ring_slot,
                                                 int64_t* const* flag_base, unsigned& bad,
-                                                T* const* part_base = nullptr, int64_t* const* pflag_base = nullptr) {
+                                                T* const* part_base = nullptr, int64_t* const* pflag_base = nullptr,
+                                                volatile long long* produced = nullptr) {
     using V = typename Tr<T>::V;
     constexpr int E = Tr<T>::EPV;
     const int lane = threadIdx.x & 31;
@@ -2627,6 +2645,11 @@ __device__ __forceinline__ unsigned nvl_produce(const LaunchParams& p, typename 
                                        p.part_version[pid]);
                     }
                 }
+                __syncwarp();
+                if (lane == 0 && produced) {  // tiles [0, kk] of this CTA are stored
+                    __threadfence_block();
+                    if (*produced < kk + 1) *produced = kk + 1;
+                }
             }
         }
         ++my_tiles;
@@ -2661,6 +2684,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     __shared__ __align__(8) uint64_t full[kNvlMaxStages];
     __shared__ __align__(8) uint64_t empty[kNvlMaxStages];
     __shared__ volatile int ready;
+    __shared__ volatile long long s_produced;  // tiles of this CTA the producers published
     // effective leaves of every plan, set after lock-in: the plan's leaves
     // (leaf pull) or its GPU-local subtree partials (hierarchical sum)
     __shared__ int eff_base[kMaxPlans + 1];
@@ -2677,6 +2701,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     if (tid == 0) {
         sm.abort = 0;
         ready = 0;
+        s_produced = 0;
         for (int st = 0; st < kNvlMaxStages; ++st) {
             mbar_init(&full[st], 1);
             mbar_init(&empty[st], kWarps);
@@ -2703,8 +2728,8 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         const long long pc0 = clock64();
         unsigned bad = 0;
         my_tiles = p.n_parts ? nvl_produce<T, kNvlDepth, true>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad,
-                                                               s_part, s_pflag0)
-                             : nvl_produce<T, kNvlDepth, false>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad);
+                                                               s_part, s_pflag0, &s_produced)
+                             : nvl_produce<T, kNvlDepth, false>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad, nullptr, nullptr, &s_produced);
         report_divergence(p, bad);
         if (p.prof && tid == 0) p.prof[blockIdx.x * 8 + 0] = clock64() - pc0;
     } else if (warp == 2 * kWarps) {
@@ -2894,6 +2919,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
                     };
                     auto own_wp = [&](int j) -> V {
                         const DevJob& jb = p.jobs[j];
+                        wait_produced(p, &s_produced, kc);
                         return __ldcg(reinterpret_cast<const V*>(ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + idx));
                     };
                     // the tree over the effective leaves: levels above the
@@ -3000,6 +3026,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     __shared__ int8_t row_of[kMaxPlans][kMaxLeaves];  // stage row of a leaf, -1: read from L2
     __shared__ int plan_rows[kMaxPlans + 1];
     __shared__ volatile int ready;
+    __shared__ volatile long long s_produced;  // tiles of this CTA the producers published
     __shared__ int64_t poll_s[kMaxPoll];
     __shared__ int plan_poll_base[kMaxPlans], plan_poll_cnt[kMaxPlans];
     __shared__ unsigned pub_count[kPubRing];
@@ -3026,6 +3053,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     if (tid == 0) {
         sm.abort = 0;
         ready = 0;
+        s_produced = 0;
         for (int st = 0; st < NSA; ++st) {
             mbar_init(&fullA[st], 1);
             mbar_init(&emptyA[st], p.red_warps);
@@ -3100,7 +3128,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     };
     if (warp < kWarps) {
         unsigned bad = 0;
-        my_tiles = nvl_produce<T, kSplitDepth>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad);
+        my_tiles = nvl_produce<T, kSplitDepth>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad, nullptr, nullptr,
+                                               &s_produced);
         report_divergence(p, bad);
         if (tid == 0) prof_set(0, clock64() - t_start);
     } else if (warp == kWarps) {
@@ -3324,6 +3353,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 }
                 auto own_wp = [&](int j) -> V {
                     const DevJob& jb = p.jobs[j];
+                    wait_produced(p, &s_produced, kc);
                     return __ldcg(reinterpret_cast<const V*>(ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) + idx));
                 };
                 finish_members<T>(p, sm, P_, acc, idx, own_wp);
