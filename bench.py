@@ -253,17 +253,28 @@ def step_bytes(a, G, gpu_index, t, elem):
     plans = [(grp, list(grp) if sync else list(tree_leaves(GroupingParams(a.P, a.S, t), grp[0]))) for grp in groups]
     hier_on = os.environ.get("WG_HIER", "0") != "0" and G >= 2
     hls = [hier_levels(leaves, R) if hier_on else 0 for _, leaves in plans]
-    split_on = os.environ.get("WG_SPLIT", "1") != "0" and G >= 2 and a.P <= 8 and not any(hls) and \
+    split_on_h = os.environ.get("WG_SPLIT", "1") != "0" and G >= 2 and a.P <= 8 and \
         n >= int(os.environ.get("WG_SPLIT_MIN_BYTES", str(8 << 20)))  # the kernel's split_min_bytes
+    split_on = split_on_h and not any(hls)
     for (grp, leaves), hl in zip(plans, hls):
         L = sum(1 for q in grp if q // R == gpu_index)
         S = len(grp)
         spans = len({q // R for q in grp})
         if hl:
             parts = leaves[::1 << hl]
+            ne = len(parts)
             local_parts = sum(1 for q in parts if q // R == gpu_index)
-            nvl += n * (len(parts) - local_parts)
-            hbm += n * local_parts
+            hbm += n * local_parts  # this GPU's partials, written once
+            pspans = len({q // R for q in parts})
+            if split_on_h and pspans >= int(os.environ.get("WG_SPLIT_SPAN", "2")) and 2 * ne >= 3 * (ne // pspans + 1):
+                # partials reduce-scattered over their keys: a fraction f of the
+                # tiles is reduced here from the other GPUs' partials, the rest
+                # arrive as one reduced tile (the reduced tiles written: f)
+                f = local_parts / ne
+                nvl += n * (f * (ne - local_parts) + (1 - f))
+                hbm += n * f
+            else:
+                nvl += n * (ne - local_parts)
         elif split_on and spans >= int(os.environ.get("WG_SPLIT_SPAN", "2")) and 2 * S >= 3 * (S // spans + 1) and \
                 len(set(leaves)) == len(leaves):
             f = L / S

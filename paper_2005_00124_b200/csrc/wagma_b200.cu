@@ -3027,6 +3027,12 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     __shared__ int plan_rows[kMaxPlans + 1];
     __shared__ volatile int ready;
     __shared__ volatile long long s_produced;  // tiles of this CTA the producers published
+    // hierarchical plans (GPU-local subtree partials as the effective leaves):
+    // owners per plan, effective leaves, tree levels above them, flag stride
+    __shared__ int8_t s_nown[kMaxPlans], s_neff[kMaxPlans], s_elog[kMaxPlans];
+    __shared__ int8_t poll_stride[kMaxPoll];
+    __shared__ T* s_part[kMaxJobs];
+    __shared__ int64_t* s_pflag0[kMaxJobs];
     __shared__ int64_t poll_s[kMaxPoll];
     __shared__ int plan_poll_base[kMaxPlans], plan_poll_cnt[kMaxPlans];
     __shared__ unsigned pub_count[kPubRing];
@@ -3076,6 +3082,15 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         }
         leaf_base[NP] = acc;
         plan_rows[NP] = rows;
+        for (int pl = 0; pl < NP; ++pl) {
+            s_nown[pl] = int8_t(p.owners[pl].n);
+            s_neff[pl] = int8_t(p.plans[pl].n_leaves);
+            s_elog[pl] = int8_t(p.plans[pl].log_leaves);
+        }
+    }
+    if (tid < p.n_parts) {
+        s_part[tid] = part_ptr<T>(p, p.part_key[tid], p.part_version[tid]);
+        s_pflag0[tid] = part_flag_ptr(p, p.part_key[tid], 0);
     }
     if (tid < kMaxVersions) sm.activator[tid] = 0;
     init_ring_slots<T>(p, s_ring, s_flag0);
@@ -3110,7 +3125,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     auto masks = [&](int kc, unsigned& ma, unsigned& mb) {
         ma = mb = 0;
         for (int pl = 0; pl < NP; ++pl) {
-            const bool remote_owner = plan_split[pl] && s_owner_remote[pl][split_owner_index(p, pl, kc)];
+            const bool remote_owner = plan_split[pl] && s_owner_remote[pl][kc % s_nown[pl]];
             (remote_owner ? mb : ma) |= 1u << pl;
         }
     };
@@ -3128,8 +3143,10 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     };
     if (warp < kWarps) {
         unsigned bad = 0;
-        my_tiles = nvl_produce<T, kSplitDepth>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad, nullptr, nullptr,
-                                               &s_produced);
+        my_tiles = p.n_parts ? nvl_produce<T, kSplitDepth, true>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad,
+                                                                 s_part, s_pflag0, &s_produced)
+                             : nvl_produce<T, kSplitDepth, false>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad,
+                                                                  nullptr, nullptr, &s_produced);
         report_divergence(p, bad);
         if (tid == 0) prof_set(0, clock64() - t_start);
     } else if (warp == kWarps) {
@@ -3145,6 +3162,44 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 plan_poll_base[pl] = n_poll;
                 // split when every member is timely, the group spans several GPUs
                 // and the split saves NVLink bytes (split_pays)
+                bool all_timely = true;
+                for (int li = 0; li < P_.n_leaves; ++li) all_timely = all_timely && sm.stamps[P_.vidx][P_.leaves[li]] == v;
+                if (p.plan_hl[pl] && all_timely) {
+                    // hierarchical: the effective leaves are the GPUs' subtree
+                    // partials (the producers' butterfly sums of 2^hl leaves),
+                    // reduce-scattered over their keys when that saves bytes
+                    const int hl = p.plan_hl[pl];
+                    const int ne = P_.n_leaves >> hl;
+                    unsigned gpus = 0;
+                    for (int u = 0; u < ne; ++u) {
+                        const int key = P_.leaves[u << hl];
+                        gpus |= 1u << (key / p.R);
+                        if (n_poll == kMaxPoll) {
+                            raise_error(p, WG_EINVAL, n_poll);
+                            break;
+                        }
+                        s_poll_ptr[n_poll] = part_flag_ptr(p, key, 0);
+                        poll_stride[n_poll] = 1;
+                        poll_s[n_poll] = v;
+                        ++n_poll;
+                        s_leaf_src[leaf_base[pl] + u] = part_ptr<T>(p, key, v);
+                    }
+                    const bool hsplit = __popc(gpus) >= p.split_span && split_pays(ne, __popc(gpus));
+                    if (hsplit) {
+                        for (int u = 0; u < ne; ++u) {
+                            const int key = P_.leaves[u << hl];
+                            s_red_base[pl][u] = red_ptr<T>(p, key, v);
+                            s_red_flag[pl][u] = red_flag_ptr(p, key, 0);
+                            s_owner_remote[pl][u] = int8_t(key / p.R != p.gpu_index);
+                        }
+                        s_nown[pl] = int8_t(ne);
+                    }
+                    s_neff[pl] = int8_t(ne);
+                    s_elog[pl] = int8_t(P_.log_leaves - hl);
+                    plan_poll_cnt[pl] = n_poll - plan_poll_base[pl];
+                    plan_split[pl] = hsplit;
+                    continue;
+                }
                 bool split = p.owners[pl].n == P_.n_leaves && p.owners[pl].n >= 2;
                 bool remote = false;
                 unsigned gpus = 0;
@@ -3165,6 +3220,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                             break;
                         }
                         s_poll_ptr[n_poll] = flag_ptr(p, q, 0, w);
+                        poll_stride[n_poll] = int8_t(kWarps);
                         poll_s[n_poll] = sm.stamps[P_.vidx][q];
                         ++n_poll;
                     }
@@ -3247,7 +3303,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                     int c = 0;
                     while (cell_pref[c + 1] <= e) ++c;
                     const int idx = plan_poll_base[c % NP] + (e - cell_pref[c]);
-                    fp[r] = s_poll_ptr[idx] + bt_tile[c / NP] * kWarps;
+                    fp[r] = s_poll_ptr[idx] + bt_tile[c / NP] * poll_stride[idx];
                     want[r] = poll_s[idx];
                     v[r] = ld_relaxed_sys(fp[r]);
                 }
@@ -3275,7 +3331,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 for (int b = 0, st = stA; b < nb; ++b) {
                     unsigned rows = 0;
                     for (int pl = 0; pl < NP; ++pl)
-                        if (bt_mask[b] >> pl & 1) rows += plan_rows[pl];
+                        if (bt_mask[b] >> pl & 1) rows += s_neff[pl] < p.plans[pl].n_leaves ? s_neff[pl] : plan_rows[pl];
                     metaA_tile[st] = bt_tile[b];
                     metaA_kc[st] = bt_kc[b];
                     metaA_mask[st] = bt_mask[b];
@@ -3290,6 +3346,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 while (leaf_base[pl + 1] <= f) ++pl;
                 if (!(bt_mask[b] >> pl & 1)) continue;
                 const int li = f - leaf_base[pl];
+                if (li >= s_neff[pl]) continue;  // hierarchical: the partials only
                 const int r = row_of[pl][li];
                 if (r < 0) continue;
                 const int st = stA + b < NSA ? stA + b : stA + b - NSA;
@@ -3346,9 +3403,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                     return __ldcg(reinterpret_cast<const V*>(
                         ring_ptr<T>(p, P_.leaves[leaf], sm.leaf_slot[pl][leaf]) + idx));
                 };
-                const V acc = tree_sum<T>(fetch, P_.log_leaves);
+                const V acc = tree_sum<T>(fetch, s_elog[pl]);
                 if (plan_split[pl]) {  // this GPU owns the tile: publish the reduced tile
-                    __stcg(reinterpret_cast<V*>(s_red_base[pl][split_owner_index(p, pl, kc)] + idx), acc);
+                    __stcg(reinterpret_cast<V*>(s_red_base[pl][kc % s_nown[pl]] + idx), acc);
                     owned = true;
                 }
                 auto own_wp = [&](int j) -> V {
@@ -3439,7 +3496,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             if (e < nb * NP && (btB_mask[e / NP] >> (e % NP) & 1)) {
                 const int pl = e % NP;
                 want = p.versions[p.plans[pl].vidx].version;
-                fp = s_red_flag[pl][split_owner_index(p, pl, btB_kc[e / NP])] + btB_tile[e / NP];
+                fp = s_red_flag[pl][btB_kc[e / NP] % s_nown[pl]] + btB_tile[e / NP];
                 x = ld_relaxed_sys(fp);
             }
             int rc = 0;
@@ -3486,7 +3543,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                 }
                 __syncwarp();
                 if (lane < NP && (mb >> lane & 1)) {
-                    const T* src = s_red_base[lane][split_owner_index(p, lane, btB_kc[bb])] + tile * p.tile_elems;
+                    const T* src = s_red_base[lane][btB_kc[bb] % s_nown[lane]] + tile * p.tile_elems;
                     bulk_g2s(ringB + (size_t(st) * NP + lane) * kThreads, src, tile_bytes, &fullB[st]);
                 }
                 __syncwarp();
@@ -3557,7 +3614,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             for (int e = lane; e < n * NP; e += 32) {
                 const int slot = int((next + e / NP) & (kRedRing - 1)), pl = e % NP;
                 if (pubq_mask[slot] >> pl & 1)
-                    st_relaxed_sys(s_red_flag[pl][split_owner_index(p, pl, pubq_kc[slot])] + pubq_tile[slot],
+                    st_relaxed_sys(s_red_flag[pl][pubq_kc[slot] % s_nown[pl]] + pubq_tile[slot],
                                    p.versions[p.plans[pl].vidx].version);
             }
             __syncwarp();
@@ -4426,6 +4483,17 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         wide = wide || (__builtin_popcount(gpus) >= ctx->split_span && p.owners[k].n == p.plans[k].n_leaves &&
                         split_pays(p.owners[k].n, __builtin_popcount(gpus)));
     }
+    // hierarchical plans whose subtree partials are worth reduce-scattering
+    // (the split kernel then sums partials; same answer on every GPU)
+    bool wide_h = false;
+    for (int k = 0; k < p.n_plans && any_hier; ++k) {
+        if (!p.plan_hl[k]) continue;
+        unsigned gpus = 0;
+        for (int li = 0; li < p.plans[k].n_leaves; ++li) gpus |= 1u << (p.plans[k].leaves[li] / ctx->R);
+        const int np = p.plans[k].n_leaves >> p.plan_hl[k];
+        wide_h = wide_h || (WG_SPLIT_TMA_LOCAL && __builtin_popcount(gpus) >= ctx->split_span &&
+                            split_pays(np, __builtin_popcount(gpus)));
+    }
     int mg_rows_in = 0, mg_cap_a = 0, mg_cap_b = 0, mg_nsi = 0;
     if (any_hier && ctx->use_mg) {
         // wagma_mg_kernel shared memory, in chunk rows: input ring (3 rows per
@@ -4464,7 +4532,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         p.loc_stages = mg_nsi;
         p.mg_cap_a = mg_cap_a;
         p.mg_cap_b = mg_cap_b;
-        p.mg_split = ctx->use_split && L_has_red(ctx);
+        p.mg_split = ctx->use_split && L_has_red(ctx) && c.n * int64_t(ctx->esize) >= ctx->split_min_bytes;
         const size_t smem_mg = size_t(mg_rows_in + mg_cap_a + mg_cap_b) * size_t(kLocChunkVecs) * 16;
         const int64_t n_chunks = (ctx->n_tiles + kLocTiles - 1) / kLocTiles;
         const int64_t g = std::min<int64_t>(n_chunks, ctx->sms);
@@ -4472,8 +4540,8 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
             wagma_mg_kernel<float><<<unsigned(g), kMgThreads, smem_mg, s>>>(p);
         else
             wagma_mg_kernel<double><<<unsigned(g), kMgThreads, smem_mg, s>>>(p);
-    } else if (p.need_fence && !any_hier && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= ctx->split_span && wide &&
-        c.n * int64_t(ctx->esize) >= ctx->split_min_bytes) {
+    } else if (p.need_fence && ctx->use_split && c.P <= kSplitMaxP && c.n_gpus >= ctx->split_span &&
+               (any_hier ? wide_h : wide) && c.n * int64_t(ctx->esize) >= ctx->split_min_bytes) {
         // split sums: every GPU of a job makes this same choice (it depends on
         // P and the process-wide knob only), so owners always publish the
         // reduced tiles their peers wait for

@@ -43,6 +43,14 @@ def test_library_is_sm100a():
 def test_error_strings_and_validation_without_gpu():
     lib = _lib.load()
     assert lib.wg_strerror(_lib.WG_ESTALE).decode().startswith("stale")
+    assert lib.wg_strerror(_lib.WG_ESYNC).decode() == "mismatched sync points"
+    assert lib.wg_strerror(_lib.WG_EDIVERGE).decode().startswith("non-finite")
+    # every code the header defines has a message and a Python constant
+    import os
+    hdr = open(os.path.join(os.path.dirname(_build.HERE), "include", "wagma_b200.h")).read()
+    for name, val in re.findall(r"#define (WG_E[A-Z]+) (\d+)", hdr):
+        assert getattr(_lib, name) == int(val), name
+        assert lib.wg_strerror(int(val)).decode() != "unknown error", name
     # invalid configs are rejected before any CUDA call
     cfg = _lib.WgConfig()
     cfg.P, cfg.S, cfg.n_gpus, cfg.n = 6, 2, 1, 10

@@ -51,8 +51,12 @@ def test_algorithmic_bytes_per_launch(monkeypatch):
     monkeypatch.setenv("WG_HIER", "1")
     hbm, nvl = b.step_bytes(a, 2, 0, 0, 4)
     assert nvl == 1.0 * N and hbm == 4 * 6 * N + N + N
-    hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)  # 4 GPUs: 2-leaf partials, pull 3
+    hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)  # 4 GPUs: 2-leaf partials, reduce-scattered: 1/4*3 + 3/4
+    assert nvl == 1.5 * N and hbm == 2 * 6 * N + N + 0.25 * N + 1.5 * N
+    monkeypatch.setenv("WG_SPLIT", "0")
+    hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)  # without the split: pull the 3 other partials
     assert nvl == 3.0 * N and hbm == 2 * 6 * N + N + 3 * N
+    monkeypatch.delenv("WG_SPLIT")
     assert b.hier_levels([0, 1, 2, 3, 4, 5, 6, 7], 4) == 2 and b.hier_levels([0, 4, 1, 5], 4) == 0
     assert b.hier_levels([0, 2, 4, 6], 4) == 1 and b.hier_levels([0, 1, 2, 3], 4) == 0  # one GPU: no exchange
     monkeypatch.setenv("WG_HIER", "0")

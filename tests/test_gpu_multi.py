@@ -41,9 +41,10 @@ def _run(tmp_path, G, port, env_extra=None, **kw):
 
 @pytest.fixture(params=["mg", "nvl-hier", "nohier"])
 def hier(request):
-    """Kernel family: hierarchical sums in the TMA-produce kernel (default),
-    hierarchical sums in the pull kernel (WG_MG=0), or no hierarchy (split /
-    pull kernels, WG_HIER=0)."""
+    """Kernel family: hierarchical sums in the TMA-produce kernel (WG_MG=1),
+    hierarchical sums in the split / pull kernels (WG_MG=0: partials
+    reduce-scattered by the split kernel where that pays, else pulled), or no
+    hierarchy (split / pull kernels over the leaves, WG_HIER=0 -- the default)."""
     return {"mg": {"WG_HIER": "1", "WG_MG": "1"}, "nvl-hier": {"WG_HIER": "1", "WG_MG": "0"},
             "nohier": {"WG_HIER": "0", "WG_MG": "1"}}[request.param]
 
