@@ -251,7 +251,7 @@ def step_bytes(a, G, gpu_index, t, elem):
             if grp not in groups:
                 groups.append(grp)
     plans = [(grp, list(grp) if sync else list(tree_leaves(GroupingParams(a.P, a.S, t), grp[0]))) for grp in groups]
-    hier_on = os.environ.get("WG_HIER", "0") != "0" and G >= 2
+    hier_on = os.environ.get("WG_HIER", "1") != "0" and G >= 2
     hls = [hier_levels(leaves, R) if hier_on else 0 for _, leaves in plans]
     split_on_h = os.environ.get("WG_SPLIT", "1") != "0" and G >= 2 and a.P <= 8 and \
         n >= int(os.environ.get("WG_SPLIT_MIN_BYTES", str(8 << 20)))  # the kernel's split_min_bytes

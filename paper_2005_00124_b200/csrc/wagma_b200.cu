@@ -3865,12 +3865,14 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     if (const char* sm = getenv("WG_SPLIT_MIN_BYTES")) ctx->split_min_bytes = std::max<long long>(0, atoll(sm));
     ctx->use_loc = 1;
     if (const char* lc = getenv("WG_LOC")) ctx->use_loc = atoi(lc);
-    // Hierarchical (GPU-local subtree) sums are opt-in: measured at P=8, n = 25.6M
-    // (profiles/r02_multigpu_ab.txt) the split / pull kernels without them are as
-    // fast at 2 GPUs and faster at 4 (S=8 0.477 ms vs 0.540 pull-hier, 0.73 mg).
-    ctx->use_hier = 0;
+    // Hierarchical (GPU-local subtree) sums where the schedule allows, in the
+    // split / pull kernels (partials reduce-scattered where that pays): measured
+    // at P=8, n = 25.6M (profiles/r02_multigpu_ab.txt) 5-7% faster than the
+    // leaf-level split / pull at 2 and 4 GPUs. The TMA-produce mg kernel is
+    // opt-in (WG_MG=1; slower: its finishers trail its producers).
+    ctx->use_hier = 1;
     if (const char* hh = getenv("WG_HIER")) ctx->use_hier = atoi(hh);
-    ctx->use_mg = 1;
+    ctx->use_mg = 0;
     if (const char* mg = getenv("WG_MG")) ctx->use_mg = atoi(mg);
     ctx->mg_nsi_max = WG_MG_IN_STAGES_MAX;
     if (const char* ns = getenv("WG_MG_NSI_MAX")) ctx->mg_nsi_max = std::max(2, atoi(ns));

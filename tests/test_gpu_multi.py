@@ -39,13 +39,13 @@ def _run(tmp_path, G, port, env_extra=None, **kw):
     return [dict(np.load(os.path.join(tmp_path, f"rank{r}.npz"))) for r in range(G)]
 
 
-@pytest.fixture(params=["mg", "nvl-hier", "nohier"])
+@pytest.fixture(params=["mg", "hier", "nohier"])
 def hier(request):
     """Kernel family: hierarchical sums in the TMA-produce kernel (WG_MG=1),
-    hierarchical sums in the split / pull kernels (WG_MG=0: partials
+    hierarchical sums in the split / pull kernels (WG_MG=0, "hier": partials
     reduce-scattered by the split kernel where that pays, else pulled), or no
-    hierarchy (split / pull kernels over the leaves, WG_HIER=0 -- the default)."""
-    return {"mg": {"WG_HIER": "1", "WG_MG": "1"}, "nvl-hier": {"WG_HIER": "1", "WG_MG": "0"},
+    hierarchy (split / pull kernels over the leaves, WG_HIER=0); "hier" is the default."""
+    return {"mg": {"WG_HIER": "1", "WG_MG": "1"}, "hier": {"WG_HIER": "1", "WG_MG": "0"},
             "nohier": {"WG_HIER": "0", "WG_MG": "1"}}[request.param]
 
 
