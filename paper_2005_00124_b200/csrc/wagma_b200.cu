@@ -1211,7 +1211,10 @@ constexpr int kSplitDepth = WG_SPLIT_DEPTH;  // producer ring depth in the split
 #define WG_SPLIT_TMA_LOCAL 1
 #endif
 constexpr int kNvlMaxStages = 16;
-constexpr int kNvlThreads = 2 * kThreads + 32;
+#ifndef WG_TMA_PRODUCE
+#define WG_TMA_PRODUCE 1
+#endif
+constexpr int kNvlThreads = 2 * kThreads + 32 + (WG_TMA_PRODUCE ? 32 : 0);  // + TMA issuer warp
 constexpr int kNvlMaxDyn = 200 * 1024;
 constexpr int kPollPerLane = 8;
 constexpr int kPullBatch = 8;  // tiles whose flags are polled and copies issued together
@@ -1348,6 +1351,25 @@ struct LocJob {
     T eta, beta;
     int32_t kind, mom;
 };
+
+// Per-job constants staged in shared memory (thread j < n_jobs).
+template <typename T>
+__device__ __forceinline__ void init_loc_jobs(const LaunchParams& p, LocJob<T>* out) {
+    const int j = threadIdx.x;
+    if (j >= p.n_jobs) return;
+    const DevJob& jb = p.jobs[j];
+    LocJob<T> lj;
+    lj.W = static_cast<T*>(jb.W);
+    lj.m = static_cast<T*>(jb.m);
+    lj.g = static_cast<const T*>(jb.g);
+    lj.fresh = static_cast<const T*>(jb.fresh);
+    lj.ring = jb.produces ? ring_ptr<T>(p, jb.rank, slot_of(p, jb.version)) : nullptr;
+    lj.eta = T(jb.eta);
+    lj.beta = T(jb.beta);
+    lj.kind = jb.kind;
+    lj.mom = jb.update_rule == WG_UPDATE_MOMENTUM;
+    out[j] = lj;
+}
 
 // Consumer work for one item (job j of a chunk): local step, m and send-ring
 // stores, W' into the thread-private stage. FULL: the chunk lies inside n.
@@ -2525,6 +2547,195 @@ __global__ void __launch_bounds__(kMgThreads, 1) wagma_mg_kernel(const __grid_co
 // readiness flags published in chunks of kPubChunk by the last warp to
 // finish a chunk (one GPU-scope fence, cumulative over the other warps'
 // stores acquired through the shared-memory counter). Never waits on a peer.
+// ---------------------------------------------------------------------------
+// TMA-fed producers of the multi-GPU kernels (WG_TMA_PRODUCE=1, defined above)
+//
+// The issuer warp's lane 0 streams W, g, m of every (tile, job) item with
+// cp.async.bulk (L2 evict-first) into a ring of NSI stages [3][kThreads]
+// guarded by mbarriers (fin: bytes landed; ein: the 8 producer warps are
+// done); the producer warps only compute: m' and W' from shared memory, m and
+// the send-ring slot stored, this GPU's subtree partials summed, the tiles'
+// flags published in chunks of kPubChunk by the last warp to finish a chunk.
+// Same per-item arithmetic and publication protocol as nvl_produce, with no
+// per-thread load issue or address arithmetic on the producers' path.
+// ---------------------------------------------------------------------------
+constexpr int kTmaMaxStages = 16;
+
+template <typename T, bool HIER>
+__device__ void tma_issue(const LaunchParams& p, typename Tr<T>::V* ring, int NSI, uint64_t* fin, uint64_t* ein,
+                          int64_t my_ntiles, const LocJob<T>* jobs) {
+    using V = typename Tr<T>::V;
+    if ((threadIdx.x & 31) != 0) return;
+    const uint64_t pol = policy_evict_first();
+    const unsigned tbytes = unsigned(kThreads) * 16u;
+    const int J = p.n_jobs;
+    int st = 0;
+    unsigned ph = 0;
+    int64_t k = 0;
+    for (int64_t kk = 0; kk < my_ntiles; ++kk) {
+        const int64_t e0 = (int64_t(blockIdx.x) + kk * gridDim.x) * p.tile_elems;
+        const int64_t rem = (p.n - e0) * int64_t(sizeof(T));
+        // caller vectors hold exactly n elements: whole 16-byte vectors by TMA,
+        // the ragged end is read by the producers from global memory
+        const unsigned bytes = rem >= tbytes ? tbytes : (rem > 0 ? unsigned(rem) & ~15u : 0u);
+        for (int jj = 0; jj < J; ++jj, ++k) {
+            const int j = HIER ? int(p.job_order[jj]) : jj;
+            if (k >= NSI && !mbar_wait(p, &ein[st], ph ^ 1u)) {
+                raise_error(p, WG_ETIMEOUT, k);
+                return;
+            }
+            const LocJob<T>& jb = jobs[j];
+            V* dst = ring + size_t(st) * 3 * kThreads;
+            if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
+                mbar_arrive_expect_tx(&fin[st], bytes);
+                if (bytes) bulk_g2s_hint(dst, jb.fresh + e0, bytes, &fin[st], pol);
+            } else {
+                mbar_arrive_expect_tx(&fin[st], (jb.mom ? 3u : 2u) * bytes);
+                if (bytes) {
+                    bulk_g2s_hint(dst, jb.W + e0, bytes, &fin[st], pol);
+                    bulk_g2s_hint(dst + kThreads, jb.g + e0, bytes, &fin[st], pol);
+                    if (jb.mom) bulk_g2s_hint(dst + 2 * kThreads, jb.m + e0, bytes, &fin[st], pol);
+                }
+            }
+            if (++st == NSI) st = 0, ph ^= 1u;
+        }
+    }
+}
+
+template <typename T, bool HIER>
+__device__ unsigned tma_produce(const LaunchParams& p, typename Tr<T>::V* ring, int NSI, uint64_t* fin,
+                                uint64_t* ein, int64_t my_ntiles, unsigned* pub_count, T* const* ring_slot,
+                                int64_t* const* flag_base, unsigned& bad, const LocJob<T>* jobs,
+                                T* const* part_base, int64_t* const* pflag_base, volatile long long* produced) {
+    using V = typename Tr<T>::V;
+    constexpr int E = Tr<T>::EPV;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int J = p.n_jobs;
+    const int NPa = HIER ? p.n_parts : 0;
+    unsigned my_tiles = 0;
+    int st = 0;
+    unsigned ph = 0;
+    for (int64_t kk = 0; kk < my_ntiles; ++kk) {
+        const int64_t tile = int64_t(blockIdx.x) + kk * gridDim.x;
+        const int64_t idx = tile * p.tile_elems + int64_t(tid) * E;
+        const bool full = idx + E <= p.n;
+        V s0, s1, s2, s3;  // butterfly stack of the partial being summed (<= 16 leaves)
+        bool ok = true;
+        for (int jj = 0; jj < J; ++jj) {
+            const int j = HIER ? int(p.job_order[jj]) : jj;
+            if (!mbar_wait(p, &fin[st], ph)) {
+                ok = false;
+                break;
+            }
+            const V* r = ring + size_t(st) * 3 * kThreads;
+            const LocJob<T>& jb = jobs[j];
+            V wp;
+            if (jb.kind == WG_JOB_GROUP_SUM || jb.kind == WG_JOB_SYNC_SUM) {
+                wp = full ? r[tid] : ld_tail(jb.fresh, idx, p.n);
+            } else {
+                const V w = full ? r[tid] : ld_tail(static_cast<const T*>(jb.W), idx, p.n);
+                const V g = full ? r[kThreads + tid] : ld_tail(jb.g, idx, p.n);
+                if (jb.mom) {
+                    // m = beta*m + g ; W' = W - eta*m  (optim.py:179,183)
+                    const V m0 = full ? r[2 * kThreads + tid] : ld_tail(static_cast<const T*>(jb.m), idx, p.n);
+                    const V mn = vadd(vscale(jb.beta, m0), g);
+                    st_stream<T>(jb.m, idx, p.n, mn);
+                    wp = vsub(w, vscale(jb.eta, mn));
+                } else {
+                    wp = vsub(w, vscale(jb.eta, g));  // W' = W - eta*g (optim.py:181-183)
+                }
+                bad |= unsigned(nonfinite(wp)) << j;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ein[st]);
+            if (++st == NSI) st = 0, ph ^= 1u;
+            if (jb.kind == WG_JOB_LOCAL_STEP) {
+                st_stream<T>(jb.W, idx, p.n, wp);
+                continue;
+            }
+            // SendBuffer.install: W' written once into the send ring
+            __stcg(reinterpret_cast<V*>(ring_slot[j] + idx), wp);
+            if (NPa && p.job_part[jj] >= 0) {
+                // partial = the subtree's butterfly sum (collective.py:321-329)
+                const int pos = p.job_ppos[jj];
+                V v = wp;
+                if (pos & 1) {
+                    v = vadd(s0, v);
+                    if (pos & 2) {
+                        v = vadd(s1, v);
+                        if (pos & 4) {
+                            v = vadd(s2, v);
+                            if (pos & 8) v = vadd(s3, v); else s3 = v;
+                        } else {
+                            s2 = v;
+                        }
+                    } else {
+                        s1 = v;
+                    }
+                } else {
+                    s0 = v;
+                }
+                if (p.job_plast[jj])
+                    __stcg(reinterpret_cast<V*>(part_base[p.job_part[jj]] + tile * p.tile_elems +
+                                                int64_t(tid) * E),
+                           v);
+            }
+        }
+        if (!ok) {
+            if (lane == 0) raise_error(p, WG_ETIMEOUT, kk);
+            break;
+        }
+        // chunk publication: the last producer warp to finish a chunk fences
+        // once (cumulative over the other warps' stores, acquired through the
+        // shared-memory counter) and raises the chunk's flags
+        const bool chunk_end = ((kk + 1) % kPubChunk == 0) || (kk + 1 == my_ntiles);
+        if (chunk_end) {
+            __syncwarp();
+            unsigned old = 0;
+            if (lane == 0) {
+                unsigned* cnt = &pub_count[(kk / kPubChunk) & (kPubRing - 1)];
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                             : "=r"(old)
+                             : "r"(smem_u32(cnt))
+                             : "memory");
+                if (old == kWarps - 1) *cnt = 0;
+            }
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old == kWarps - 1) {
+                if (p.fence_scope == 0)
+                    fence_sys();
+                else if (p.fence_scope == 1)
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                const int64_t k0 = kk - (kk % kPubChunk);
+                const int nk = int(kk - k0 + 1);
+                for (int e = lane; e < nk * J * kWarps; e += 32) {
+                    const int w = e % kWarps, j = (e / kWarps) % J, b = e / (kWarps * J);
+                    const DevJob& djb = p.jobs[j];
+                    if (djb.produces)
+                        st_relaxed_sys(flag_base[j] + (int64_t(blockIdx.x) + (k0 + b) * gridDim.x) * kWarps + w,
+                                       djb.version);
+                }
+                if constexpr (HIER) {
+                    for (int e = lane; e < nk * NPa; e += 32) {
+                        const int pid = e % NPa, b = e / NPa;
+                        st_relaxed_sys(pflag_base[pid] + int64_t(blockIdx.x) + (k0 + b) * gridDim.x,
+                                       p.part_version[pid]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0 && produced) {
+                    __threadfence_block();
+                    if (*produced < kk + 1) *produced = kk + 1;
+                }
+            }
+        }
+        ++my_tiles;
+        // warps cannot drift more than the input ring apart (every stage waits
+        // for all 8 producer warps), far less than the counter ring
+    }
+    return my_tiles;
+}
+
 // A late member's own W' of this launch is read back from its send slot by
 // the consumer warps (finish_members' own_wp). When every leaf of its group
 // is a complete older slot or lives on another GPU, no polled flag orders
@@ -2685,6 +2896,8 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     __shared__ __align__(8) uint64_t empty[kNvlMaxStages];
     __shared__ volatile int ready;
     __shared__ volatile long long s_produced;  // tiles of this CTA the producers published
+    __shared__ __align__(8) uint64_t s_fin[kTmaMaxStages], s_ein[kTmaMaxStages];  // TMA input ring
+    __shared__ LocJob<T> s_pj[kMaxJobs];
     // effective leaves of every plan, set after lock-in: the plan's leaves
     // (leaf pull) or its GPU-local subtree partials (hierarchical sum)
     __shared__ int eff_base[kMaxPlans + 1];
@@ -2702,6 +2915,10 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         sm.abort = 0;
         ready = 0;
         s_produced = 0;
+        for (int st = 0; st < kNvlDepth; ++st) {
+            mbar_init(&s_fin[st], 1);
+            mbar_init(&s_ein[st], kWarps);
+        }
         for (int st = 0; st < kNvlMaxStages; ++st) {
             mbar_init(&full[st], 1);
             mbar_init(&empty[st], kWarps);
@@ -2709,6 +2926,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
     }
     if (tid < kMaxVersions) sm.activator[tid] = 0;
     init_ring_slots<T>(p, s_ring, s_flag0);
+    init_loc_jobs<T>(p, s_pj);
     if (tid < p.n_parts) {
         s_part[tid] = part_ptr<T>(p, p.part_key[tid], p.part_version[tid]);
         s_pflag0[tid] = part_flag_ptr(p, p.part_key[tid], 0);
@@ -2727,11 +2945,25 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         // ---------------- producers ----------------
         const long long pc0 = clock64();
         unsigned bad = 0;
-        my_tiles = p.n_parts ? nvl_produce<T, kNvlDepth, true>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad,
-                                                               s_part, s_pflag0, &s_produced)
-                             : nvl_produce<T, kNvlDepth, false>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad, nullptr, nullptr, &s_produced);
+        if (WG_TMA_PRODUCE)
+            my_tiles = p.n_parts ? tma_produce<T, true>(p, ring, kNvlDepth, s_fin, s_ein, my_ntiles, pub_count, s_ring,
+                                                        s_flag0, bad, s_pj, s_part, s_pflag0, &s_produced)
+                                 : tma_produce<T, false>(p, ring, kNvlDepth, s_fin, s_ein, my_ntiles, pub_count, s_ring,
+                                                         s_flag0, bad, s_pj, nullptr, nullptr, &s_produced);
+        else
+            my_tiles = p.n_parts ? nvl_produce<T, kNvlDepth, true>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad,
+                                                                   s_part, s_pflag0, &s_produced)
+                                 : nvl_produce<T, kNvlDepth, false>(p, ring, my_ntiles, pub_count, s_ring, s_flag0,
+                                                                    bad, nullptr, nullptr, &s_produced);
         report_divergence(p, bad);
         if (p.prof && tid == 0) p.prof[blockIdx.x * 8 + 0] = clock64() - pc0;
+    } else if (WG_TMA_PRODUCE && warp == 2 * kWarps + 1) {
+        // ---------------- TMA input issuer ----------------
+        if (p.n_parts)
+            tma_issue<T, true>(p, ring, kNvlDepth, s_fin, s_ein, my_ntiles, s_pj);
+        else
+            tma_issue<T, false>(p, ring, kNvlDepth, s_fin, s_ein, my_ntiles, s_pj);
+        my_tiles = 0;
     } else if (warp == 2 * kWarps) {
         // ---------------- puller ----------------
         if (blockIdx.x == 0) control_phase(p, sm.activator);
@@ -2978,7 +3210,8 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
 // so no cross-GPU wait cycle exists.
 // ---------------------------------------------------------------------------
 
-constexpr int kSplitThreads = 23 * 32;  // + 1 publisher warp (reduced-tile fences and flags)
+constexpr int kSplitPubWarp = 22;  // publisher warp (reduced-tile fences and flags)
+constexpr int kSplitThreads = (23 + (WG_TMA_PRODUCE ? 1 : 0)) * 32;  // + TMA issuer warp (warp 23)
 // puller wait counters for tools/phase_profile.py (off: they cost registers)
 #ifdef WG_PROF_COUNTERS
 #define WG_PCNT(...) __VA_ARGS__
@@ -3033,6 +3266,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     __shared__ int8_t poll_stride[kMaxPoll];
     __shared__ T* s_part[kMaxJobs];
     __shared__ int64_t* s_pflag0[kMaxJobs];
+    __shared__ __align__(8) uint64_t s_fin[kTmaMaxStages], s_ein[kTmaMaxStages];  // TMA input ring
+    __shared__ LocJob<T> s_pj[kMaxJobs];
     __shared__ int64_t poll_s[kMaxPoll];
     __shared__ int plan_poll_base[kMaxPlans], plan_poll_cnt[kMaxPlans];
     __shared__ unsigned pub_count[kPubRing];
@@ -3060,6 +3295,10 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
         sm.abort = 0;
         ready = 0;
         s_produced = 0;
+        for (int st = 0; st < kSplitDepth; ++st) {
+            mbar_init(&s_fin[st], 1);
+            mbar_init(&s_ein[st], kWarps);
+        }
         for (int st = 0; st < NSA; ++st) {
             mbar_init(&fullA[st], 1);
             mbar_init(&emptyA[st], p.red_warps);
@@ -3094,6 +3333,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     }
     if (tid < kMaxVersions) sm.activator[tid] = 0;
     init_ring_slots<T>(p, s_ring, s_flag0);
+    init_loc_jobs<T>(p, s_pj);
     if (tid < kPubRing) pub_count[tid] = 0;
     if (tid < kRedRing) {
         red_count[tid] = 0;
@@ -3143,12 +3383,24 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     };
     if (warp < kWarps) {
         unsigned bad = 0;
-        my_tiles = p.n_parts ? nvl_produce<T, kSplitDepth, true>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad,
-                                                                 s_part, s_pflag0, &s_produced)
-                             : nvl_produce<T, kSplitDepth, false>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad,
-                                                                  nullptr, nullptr, &s_produced);
+        if (WG_TMA_PRODUCE)
+            my_tiles = p.n_parts ? tma_produce<T, true>(p, ring, kSplitDepth, s_fin, s_ein, my_ntiles, pub_count,
+                                                        s_ring, s_flag0, bad, s_pj, s_part, s_pflag0, &s_produced)
+                                 : tma_produce<T, false>(p, ring, kSplitDepth, s_fin, s_ein, my_ntiles, pub_count,
+                                                         s_ring, s_flag0, bad, s_pj, nullptr, nullptr, &s_produced);
+        else
+            my_tiles = p.n_parts ? nvl_produce<T, kSplitDepth, true>(p, ring, my_ntiles, pub_count, s_ring, s_flag0,
+                                                                     bad, s_part, s_pflag0, &s_produced)
+                                 : nvl_produce<T, kSplitDepth, false>(p, ring, my_ntiles, pub_count, s_ring, s_flag0,
+                                                                      bad, nullptr, nullptr, &s_produced);
         report_divergence(p, bad);
         if (tid == 0) prof_set(0, clock64() - t_start);
+    } else if (WG_TMA_PRODUCE && warp == kSplitPubWarp + 1) {
+        // ---------------- TMA input issuer ----------------
+        if (p.n_parts)
+            tma_issue<T, true>(p, ring, kSplitDepth, s_fin, s_ein, my_ntiles, s_pj);
+        else
+            tma_issue<T, false>(p, ring, kSplitDepth, s_fin, s_ein, my_ntiles, s_pj);
     } else if (warp == kWarps) {
         // ---------------- stream A puller ----------------
         if (blockIdx.x == 0) control_phase(p, sm.activator);
@@ -3561,7 +3813,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
             prof_set(5, clock64() - t_start);
             WG_PCNT(prof_set(11, b_empty); prof_set(12, b_poll); prof_set(13, b_notready);)
         }
-    } else if (warp == kSplitThreads / 32 - 1) {
+    } else if (warp == kSplitPubWarp) {
         // ---------------- publisher ----------------
         // Owned reduced tiles, in order: every run of consecutive ready tiles
         // gets one fence (cumulative over the reducers' stores, acquired
