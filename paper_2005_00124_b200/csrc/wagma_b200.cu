@@ -157,7 +157,8 @@ struct LaunchParams {
     int32_t loc_stages;   // single-GPU TMA kernel: input-ring stages
     int64_t* err_host;    // host-mapped mirror of the error word (wg_ctx_error_async)
     int32_t mg_cap_a, mg_cap_b;  // wagma_mg_kernel: phase-1 / phase-2 row capacity (chunk rows)
-    int32_t mg_split, pad_mg;    // wagma_mg_kernel: split (reduce-scatter) partial sums where they pay
+    int32_t mg_split;            // wagma_mg_kernel: split (reduce-scatter) partial sums where they pay
+    int32_t tma_prod;            // wagma_nvl_kernel: TMA-fed producers (else per-thread cp.async rings)
     // hierarchical sums (multi-GPU pull kernel): a plan whose lowest plan_hl
     // tree levels stay inside one GPU exchanges GPU-local subtree partials
     // instead of leaves when all its members are timely
@@ -1185,7 +1186,7 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
 // ---------------------------------------------------------------------------
 
 #ifndef WG_NVL_DEPTH
-#define WG_NVL_DEPTH 3
+#define WG_NVL_DEPTH 5
 #endif
 #ifndef WG_NVL_TMA_LOCAL
 #define WG_NVL_TMA_LOCAL 1
@@ -1211,8 +1212,15 @@ constexpr int kSplitDepth = WG_SPLIT_DEPTH;  // producer ring depth in the split
 #define WG_SPLIT_TMA_LOCAL 1
 #endif
 constexpr int kNvlMaxStages = 16;
+// TMA-fed producers (an issuer warp streams the inputs by cp.async.bulk): in
+// the pull kernel for launches of >= 2 jobs per GPU (measured 2 GPUs P=8 S=8
+// 0.588 -> 0.552 ms with a 5-deep ring; one job per GPU stays on the cp.async
+// rings, 0.235 vs 0.249 ms); not in the split kernel (4 GPUs S=8 0.450 vs 0.477)
 #ifndef WG_TMA_PRODUCE
 #define WG_TMA_PRODUCE 1
+#endif
+#ifndef WG_TMA_PRODUCE_SPLIT
+#define WG_TMA_PRODUCE_SPLIT 0
 #endif
 constexpr int kNvlThreads = 2 * kThreads + 32 + (WG_TMA_PRODUCE ? 32 : 0);  // + TMA issuer warp
 constexpr int kNvlMaxDyn = 200 * 1024;
@@ -2945,7 +2953,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         // ---------------- producers ----------------
         const long long pc0 = clock64();
         unsigned bad = 0;
-        if (WG_TMA_PRODUCE)
+        if (WG_TMA_PRODUCE && p.tma_prod)
             my_tiles = p.n_parts ? tma_produce<T, true>(p, ring, kNvlDepth, s_fin, s_ein, my_ntiles, pub_count, s_ring,
                                                         s_flag0, bad, s_pj, s_part, s_pflag0, &s_produced)
                                  : tma_produce<T, false>(p, ring, kNvlDepth, s_fin, s_ein, my_ntiles, pub_count, s_ring,
@@ -2959,7 +2967,9 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
         if (p.prof && tid == 0) p.prof[blockIdx.x * 8 + 0] = clock64() - pc0;
     } else if (WG_TMA_PRODUCE && warp == 2 * kWarps + 1) {
         // ---------------- TMA input issuer ----------------
-        if (p.n_parts)
+        if (!p.tma_prod)
+            ;
+        else if (p.n_parts)
             tma_issue<T, true>(p, ring, kNvlDepth, s_fin, s_ein, my_ntiles, s_pj);
         else
             tma_issue<T, false>(p, ring, kNvlDepth, s_fin, s_ein, my_ntiles, s_pj);
@@ -3211,7 +3221,7 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
 // ---------------------------------------------------------------------------
 
 constexpr int kSplitPubWarp = 22;  // publisher warp (reduced-tile fences and flags)
-constexpr int kSplitThreads = (23 + (WG_TMA_PRODUCE ? 1 : 0)) * 32;  // + TMA issuer warp (warp 23)
+constexpr int kSplitThreads = (23 + (WG_TMA_PRODUCE_SPLIT ? 1 : 0)) * 32;  // + TMA issuer warp (warp 23)
 // puller wait counters for tools/phase_profile.py (off: they cost registers)
 #ifdef WG_PROF_COUNTERS
 #define WG_PCNT(...) __VA_ARGS__
@@ -3383,7 +3393,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
     };
     if (warp < kWarps) {
         unsigned bad = 0;
-        if (WG_TMA_PRODUCE)
+        if (WG_TMA_PRODUCE_SPLIT)
             my_tiles = p.n_parts ? tma_produce<T, true>(p, ring, kSplitDepth, s_fin, s_ein, my_ntiles, pub_count,
                                                         s_ring, s_flag0, bad, s_pj, s_part, s_pflag0, &s_produced)
                                  : tma_produce<T, false>(p, ring, kSplitDepth, s_fin, s_ein, my_ntiles, pub_count,
@@ -3395,7 +3405,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1) wagma_split_kernel(const __g
                                                                       bad, nullptr, nullptr, &s_produced);
         report_divergence(p, bad);
         if (tid == 0) prof_set(0, clock64() - t_start);
-    } else if (WG_TMA_PRODUCE && warp == kSplitPubWarp + 1) {
+    } else if (WG_TMA_PRODUCE_SPLIT && warp == kSplitPubWarp + 1) {
         // ---------------- TMA input issuer ----------------
         if (p.n_parts)
             tma_issue<T, true>(p, ring, kSplitDepth, s_fin, s_ein, my_ntiles, s_pj);
@@ -4847,6 +4857,7 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         n_leaves_total <= kMaxPlans * kMaxLeaves) {
         p.nvl_stages = nvl_stages;
         p.nvl_rows = n_rows;
+        p.tma_prod = n_jobs >= 2;
         const size_t nvl_smem = nvl_fixed + size_t(nvl_stages) * n_rows * row;
         const int di = c.dtype == WG_F32 ? 0 : 1;
         if (ctx->occ_nvl[di] <= 0) {
