@@ -14,3 +14,7 @@ done
 timeout 600 python bench.py --impl reference > gpurun_out/rf_ref_n1.json 2> gpurun_out/rf_ref_n1.err
 for N in 1 2 4; do python -c "import json; d=json.load(open('gpurun_out/rf_bench_n$N.json')); print($N, round(d['value'],1), d['unit'], round(d['ms_per_step'],4), d['roofline']['bound'], round(d['roofline']['frac'],3), 'e2e', d['e2e']['value'] if d.get('e2e') else None, d['clocks'])"; done
 python -c "import json; d=json.load(open('gpurun_out/rf_ref_n1.json')); print('reference', d['value'], d['cpu_baseline']['cores'])"
+{
+bash tools/ab_env.sh 2 "-|WG_HIER=0" --P 2 --S 2
+bash tools/ab_env.sh 4 "-" --S 4
+} > gpurun_out/rf_extra.txt 2>&1; cat gpurun_out/rf_extra.txt
