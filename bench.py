@@ -255,6 +255,18 @@ def step_bytes(a, G, gpu_index, t, elem):
     hls = [hier_levels(leaves, R) if hier_on else 0 for _, leaves in plans]
     split_on_h = os.environ.get("WG_SPLIT", "1") != "0" and G >= 2 and a.P <= 8 and \
         n >= int(os.environ.get("WG_SPLIT_MIN_BYTES", str(8 << 20)))  # the kernel's split_min_bytes
+    # the kernel sums leaves when its partials would be reduce-scattered and the
+    # replica exceeds WG_HIER_SPLIT_MAX_BYTES (mirrors wg_launch)
+    span_min = int(os.environ.get("WG_SPLIT_SPAN", "2"))
+
+    def pays(leaves, hl):
+        parts = leaves[::1 << hl]
+        sp = len({q // R for q in parts})
+        return sp >= span_min and 2 * len(parts) >= 3 * (len(parts) // sp + 1)
+    wide_h = any(hl and pays(leaves, hl) for (_, leaves), hl in zip(plans, hls))
+    if wide_h and os.environ.get("WG_MG", "0") == "0" and \
+            n > int(os.environ.get("WG_HIER_SPLIT_MAX_BYTES", str(160 << 20))):
+        hls = [0] * len(hls)
     split_on = split_on_h and not any(hls)
     for (grp, leaves), hl in zip(plans, hls):
         L = sum(1 for q in grp if q // R == gpu_index)

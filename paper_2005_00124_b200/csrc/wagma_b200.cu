@@ -4033,7 +4033,7 @@ struct Blob {
     // its tile ownership (grid = SMs x occupancy) and the flag fence scope
     int32_t use_nvl, use_split, split_span, fence_scope, sms, occ_split, occ_nvl, use_hier;
     int32_t use_mg, pad_b;
-    int64_t split_min_bytes;
+    int64_t split_min_bytes, hier_split_max_bytes;
     cudaIpcMemHandle_t handle;
 };
 constexpr uint64_t kBlobMagic = 0x57474d4142323030ull;  // "WGMAB200"
@@ -4068,6 +4068,7 @@ struct wg_ctx {
     int use_hier;             // multi-GPU: exchange GPU-local subtree partials where the tree allows
     int use_mg;               // hierarchical launches: the TMA-produce multi-GPU kernel (else the pull kernel)
     int mg_nsi_max;           // wagma_mg_kernel: deepest input ring tried (WG_MG_NSI_MAX)
+    int64_t hier_split_max_bytes;  // reduce-scattered partials only up to this replica size
     int mg_dyn_max[2];        // dynamic shared memory available to wagma_mg_kernel<T>
     int adaptive_grace;       // activator skips the grace wait for ranks late at the previous version
     int loc_dyn_max[2];       // dynamic shared memory available to wagma_local_kernel<T>
@@ -4136,6 +4137,8 @@ int wg_ctx_create(const wg_config* cfg, wg_ctx** out) {
     if (const char* hh = getenv("WG_HIER")) ctx->use_hier = atoi(hh);
     ctx->use_mg = 0;
     if (const char* mg = getenv("WG_MG")) ctx->use_mg = atoi(mg);
+    ctx->hier_split_max_bytes = int64_t(160) << 20;
+    if (const char* hm = getenv("WG_HIER_SPLIT_MAX_BYTES")) ctx->hier_split_max_bytes = std::max<long long>(0, atoll(hm));
     ctx->mg_nsi_max = WG_MG_IN_STAGES_MAX;
     if (const char* ns = getenv("WG_MG_NSI_MAX")) ctx->mg_nsi_max = std::max(2, atoi(ns));
     ctx->adaptive_grace = 1;
@@ -4316,6 +4319,7 @@ int wg_ctx_export(wg_ctx* ctx, void* blob, size_t cap, size_t* len) {
     b.occ_split = ctx->occ_split[ctx->cfg.dtype == WG_F32 ? 0 : 1];
     b.occ_nvl = ctx->occ_nvl[ctx->cfg.dtype == WG_F32 ? 0 : 1];
     b.split_min_bytes = ctx->split_min_bytes;
+    b.hier_split_max_bytes = ctx->hier_split_max_bytes;
     b.use_hier = ctx->use_hier;
     b.use_mg = ctx->use_mg;
     WG_CUDA(cudaSetDevice(ctx->cfg.device));
@@ -4340,6 +4344,7 @@ int wg_ctx_import_peer(wg_ctx* ctx, int gpu_index, const void* blob, size_t len)
     if (b.use_nvl != ctx->use_nvl || b.use_split != ctx->use_split || b.split_span != ctx->split_span ||
         b.fence_scope != ctx->fence_scope || b.sms != ctx->sms || b.occ_split != ctx->occ_split[di] ||
         b.occ_nvl != ctx->occ_nvl[di] || b.split_min_bytes != ctx->split_min_bytes || b.use_hier != ctx->use_hier ||
+        b.hier_split_max_bytes != ctx->hier_split_max_bytes ||
         b.use_mg != ctx->use_mg)
         return fail(WG_EINVAL,
                     "peer %d runs different kernel settings (WG_NVL/WG_SPLIT/WG_SPLIT_SPAN/WG_SPLIT_MIN_BYTES/"
@@ -4757,6 +4762,20 @@ int wg_launch(wg_ctx* ctx, const wg_job* jobs, int n_jobs, const int64_t* forced
         const int np = p.plans[k].n_leaves >> p.plan_hl[k];
         wide_h = wide_h || (WG_SPLIT_TMA_LOCAL && __builtin_popcount(gpus) >= ctx->split_span &&
                             split_pays(np, __builtin_popcount(gpus)));
+    }
+    // Large replicas: reduce-scattering the partials (4+ GPUs) measured slower
+    // than the leaf-level split (4 GPUs, S=8: 268 MB 1.104 vs 1.065 ms, 852 MB
+    // 3.39 vs 3.09 ms; 102 MB 0.453 vs 0.483 ms): above hier_split_max_bytes such
+    // a launch sums leaves (same decision on every GPU: it depends on the schedule)
+    if (any_hier && wide_h && !ctx->use_mg && c.n * int64_t(ctx->esize) > ctx->hier_split_max_bytes) {
+        any_hier = false;
+        wide_h = false;
+        for (int j = 0; j < n_jobs; ++j) {
+            p.job_order[j] = int8_t(j);
+            p.job_part[j] = -1;
+        }
+        for (int k = 0; k < p.n_plans; ++k) p.plan_hl[k] = 0;
+        p.n_parts = 0;
     }
     int mg_rows_in = 0, mg_cap_a = 0, mg_cap_b = 0, mg_nsi = 0;
     if (any_hier && ctx->use_mg) {

@@ -70,3 +70,22 @@ def test_algorithmic_bytes_per_launch(monkeypatch):
     a = types.SimpleNamespace(P=4, S=4, tau=10, n=262_144)  # 1 MiB: below the split threshold
     hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)
     assert nvl == 3 * 4.0 * 262_144
+
+
+def test_large_replicas_sum_leaves_at_four_gpus(monkeypatch):
+    """Above WG_HIER_SPLIT_MAX_BYTES (160 MiB) a launch whose partials would be
+    reduce-scattered sums leaves instead (wg_launch); 2 GPUs keep the partials."""
+    import types
+
+    b = _bench_module()
+    n = 213_000_000
+    N = 4.0 * n
+    a = types.SimpleNamespace(P=8, S=8, tau=8, n=n)
+    monkeypatch.delenv("WG_HIER", raising=False)
+    hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)  # leaf-level split: 2.25 N
+    assert nvl == 2.25 * N
+    hbm, nvl = b.step_bytes(a, 2, 0, 0, 4)  # 2 GPUs: pull the other GPU's partial
+    assert nvl == 1.0 * N
+    monkeypatch.setenv("WG_HIER_SPLIT_MAX_BYTES", str(1 << 40))
+    hbm, nvl = b.step_bytes(a, 4, 0, 0, 4)
+    assert nvl == 1.5 * N
