@@ -1191,7 +1191,11 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
 #ifndef WG_NVL_TMA_LOCAL
 #define WG_NVL_TMA_LOCAL 1
 #endif
-constexpr int kNvlDepth = WG_NVL_DEPTH;  // producer cp.async ring depth (items)
+constexpr int kNvlDepth = WG_NVL_DEPTH;  // producer input ring (items): the TMA ring's stages
+#ifndef WG_NVL_DEPTH_CPA
+#define WG_NVL_DEPTH_CPA 3
+#endif
+constexpr int kNvlDepthCpa = WG_NVL_DEPTH_CPA < WG_NVL_DEPTH ? WG_NVL_DEPTH_CPA : WG_NVL_DEPTH;  // per-thread cp.async ring (one job per GPU)
 #ifndef WG_SPLIT_DEPTH
 #define WG_SPLIT_DEPTH 3
 #endif
@@ -2959,9 +2963,9 @@ __global__ void __launch_bounds__(kNvlThreads, 1) wagma_nvl_kernel(const __grid_
                                  : tma_produce<T, false>(p, ring, kNvlDepth, s_fin, s_ein, my_ntiles, pub_count, s_ring,
                                                          s_flag0, bad, s_pj, nullptr, nullptr, &s_produced);
         else
-            my_tiles = p.n_parts ? nvl_produce<T, kNvlDepth, true>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad,
+            my_tiles = p.n_parts ? nvl_produce<T, kNvlDepthCpa, true>(p, ring, my_ntiles, pub_count, s_ring, s_flag0, bad,
                                                                    s_part, s_pflag0, &s_produced)
-                                 : nvl_produce<T, kNvlDepth, false>(p, ring, my_ntiles, pub_count, s_ring, s_flag0,
+                                 : nvl_produce<T, kNvlDepthCpa, false>(p, ring, my_ntiles, pub_count, s_ring, s_flag0,
                                                                     bad, nullptr, nullptr, &s_produced);
         report_divergence(p, bad);
         if (p.prof && tid == 0) p.prof[blockIdx.x * 8 + 0] = clock64() - pc0;
