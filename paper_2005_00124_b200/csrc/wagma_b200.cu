@@ -2758,7 +2758,13 @@ __device__ __forceinline__ void wait_produced(const LaunchParams& p, const volat
         const uint64_t t0 = globaltimer();
         int it = 0;
         while (*produced <= kc) {
-            if ((++it & 255) == 0 && (globaltimer() - t0 > uint64_t(p.timeout_ns) || aborted(p))) break;
+            if ((++it & 255) == 0) {
+                if (aborted(p)) break;  // the producers latched an error: results are void
+                if (globaltimer() - t0 > uint64_t(p.timeout_ns)) {
+                    raise_error(p, WG_ETIMEOUT, kc);
+                    break;
+                }
+            }
             __nanosleep(32);
         }
     }
