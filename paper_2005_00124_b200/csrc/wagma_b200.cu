@@ -201,6 +201,44 @@ __device__ __forceinline__ int64_t atom_cas_sys(int64_t* p, int64_t cmp, int64_t
     return old;
 }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+// Control words (announce, descriptors, slot completion, sync marks) at the
+// narrowest correct scope: system scope when peers on other GPUs take part,
+// GPU scope for a single-GPU context (every reader runs on this GPU; the host
+// reads them only after the stream synchronised; the host-mapped error mirror
+// stays system scope). A system-scope fence costs ~5 us.
+__device__ __forceinline__ int64_t ld_acquire_sc(bool sys, const int64_t* p) {
+    if (sys) return ld_acquire_sys(p);
+    int64_t v;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sc(bool sys, int64_t* p, int64_t v) {
+    if (sys)
+        st_release_sys(p, v);
+    else
+        asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sc(bool sys, int64_t* p, int64_t v) {
+    if (sys)
+        st_relaxed_sys(p, v);
+    else
+        asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int64_t atom_cas_sc(bool sys, int64_t* p, int64_t cmp, int64_t val) {
+    if (sys) return atom_cas_sys(p, cmp, val);
+    int64_t old;
+    asm volatile("atom.acq_rel.gpu.global.cas.b64 %0, [%1], %2, %3;"
+                 : "=l"(old)
+                 : "l"(p), "l"(cmp), "l"(val)
+                 : "memory");
+    return old;
+}
+__device__ __forceinline__ void fence_sc(bool sys) {
+    if (sys)
+        fence_sys();
+    else
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -367,7 +405,7 @@ __device__ __forceinline__ bool aborted(const LaunchParams& p) {
 // Spin until *addr == want. Returns 0 ok, WG_EPROTO if the word moved past
 // `want` (slot reused / descriptor recycled), WG_ETIMEOUT on the watchdog.
 __device__ int spin_eq(const LaunchParams& p, const int64_t* addr, int64_t want, uint64_t t0) {
-    int64_t v = ld_acquire_sys(addr);
+    int64_t v = ld_acquire_sc(p.G > 1, addr);
     int it = 0;
     while (v != want) {
         if (v > want) return WG_EPROTO;
@@ -376,7 +414,7 @@ __device__ int spin_eq(const LaunchParams& p, const int64_t* addr, int64_t want,
             if (aborted(p)) return WG_ETIMEOUT;
         }
         __nanosleep(64);
-        v = ld_acquire_sys(addr);
+        v = ld_acquire_sc(p.G > 1, addr);
     }
     return 0;
 }
@@ -411,11 +449,11 @@ __device__ void control_phase(const LaunchParams& p, int* s_activator) {
             if (!jb.produces) continue;
             // how this rank joins version v (global sync or group round): the
             // sync-point check of every consumer (check_sync_points)
-            st_relaxed_sys(syncmark_ptr(p, jb.rank, slot_of(p, jb.version)),
+            st_relaxed_sc(p.G > 1, syncmark_ptr(p, jb.rank, slot_of(p, jb.version)),
                            2 * (jb.version + 1) + (p.versions[jb.vidx].mode == kSync));
-            st_release_sys(announce_ptr(p, jb.rank), jb.version);
+            st_release_sc(p.G > 1, announce_ptr(p, jb.rank), jb.version);
         }
-        fence_sys();
+        fence_sc(p.G > 1);
     }
     __syncwarp();
     for (int vi = 0; vi < p.n_versions; ++vi) {
@@ -427,7 +465,7 @@ __device__ void control_phase(const LaunchParams& p, int* s_activator) {
         if (lane == 0) {
             // First arrival raises the activation flag (collective.py:214-218);
             // later arrivals find it raised (exactly-once, collective.py:236).
-            int64_t st = ld_acquire_sys(&d->state);
+            int64_t st = ld_acquire_sc(p.G > 1, &d->state);
             for (;;) {
                 const int64_t sv = st / 4 - 1;
                 if (sv == v) break;
@@ -435,7 +473,7 @@ __device__ void control_phase(const LaunchParams& p, int* s_activator) {
                     raise_error(p, WG_EPROTO, v);
                     break;
                 }
-                const int64_t old = atom_cas_sys(&d->state, st, (v + 1) * 4 + 1);
+                const int64_t old = atom_cas_sc(p.G > 1, &d->state, st, (v + 1) * 4 + 1);
                 if (old == st) {
                     act = 1;
                     break;
@@ -464,18 +502,18 @@ __device__ void control_phase(const LaunchParams& p, int* s_activator) {
         const int q0 = lane, q1 = lane + 32;
         bool skip0 = false, skip1 = false;
         if (p.adaptive_grace) {
-            skip0 = q0 < p.P && ld_acquire_sys(announce_ptr(p, q0)) < v - 1;
-            skip1 = q1 < p.P && ld_acquire_sys(announce_ptr(p, q1)) < v - 1;
+            skip0 = q0 < p.P && ld_acquire_sc(p.G > 1, announce_ptr(p, q0)) < v - 1;
+            skip1 = q1 < p.P && ld_acquire_sc(p.G > 1, announce_ptr(p, q1)) < v - 1;
         }
         int64_t a0 = kNever, a1 = kNever;
         for (;;) {
             bool in = true;
             if (q0 < p.P) {
-                a0 = ld_acquire_sys(announce_ptr(p, q0));
+                a0 = ld_acquire_sc(p.G > 1, announce_ptr(p, q0));
                 if (a0 < v && q0 / p.R != p.gpu_index && !skip0) in = false;
             }
             if (q1 < p.P) {
-                a1 = ld_acquire_sys(announce_ptr(p, q1));
+                a1 = ld_acquire_sc(p.G > 1, announce_ptr(p, q1));
                 if (a1 < v && q1 / p.R != p.gpu_index && !skip1) in = false;
             }
             if (__all_sync(0xffffffffu, in)) break;
@@ -497,8 +535,8 @@ __device__ void control_phase(const LaunchParams& p, int* s_activator) {
         }
         __syncwarp();
         if (lane == 0) {
-            fence_sys();
-            st_release_sys(&d->state, (v + 1) * 4 + 2);
+            fence_sc(p.G > 1);
+            st_release_sc(p.G > 1, &d->state, (v + 1) * 4 + 2);
         }
         __syncwarp();
     }
@@ -551,14 +589,14 @@ __device__ void check_sync_points(const LaunchParams& p, const SmemCtl& sm) {
         const int slot = slot_of(p, v);
         for (int q = lane; q < p.P; q += 32) {
             const int64_t* mk = syncmark_ptr(p, q, slot);
-            int64_t x = ld_acquire_sys(mk);
+            int64_t x = ld_acquire_sc(p.G > 1, mk);
             if (sync) {
                 const uint64_t t0 = globaltimer();
                 int it = 0;
                 while (x < 2 * (v + 1)) {
                     if ((++it & 63) == 0 && (globaltimer() - t0 > uint64_t(p.timeout_ns) || aborted(p))) break;
                     __nanosleep(64);
-                    x = ld_acquire_sys(mk);
+                    x = ld_acquire_sc(p.G > 1, mk);
                 }
                 if (x == 2 * (v + 1)) raise_error(p, WG_ESYNC, v * 1024 + q);
             } else if (sm.stamps[vi][q] == v && x == 2 * (v + 1) + 1) {
@@ -620,7 +658,7 @@ __device__ bool resolve_core(const LaunchParams& p, SmemCtl& sm, int tid, int nt
                 raise_error(p, WG_EPROTO, s);  // slot overwritten in this launch
                 sm.abort = 1;
             }
-            const int64_t c = ld_acquire_sys(complete_ptr(p, q, slot));
+            const int64_t c = ld_acquire_sc(p.G > 1, complete_ptr(p, q, slot));
             if (c > s) {
                 raise_error(p, WG_EPROTO, s);  // send ring wrapped past the stamp
                 sm.abort = 1;
@@ -879,12 +917,12 @@ __device__ __forceinline__ void publish_slots(const LaunchParams& p, unsigned my
     if (j < p.n_jobs && p.jobs[j].produces && my_tiles) {
         const DevJob& jb = p.jobs[j];
         const int slot = slot_of(p, jb.version);
-        fence_sys();
+        fence_sc(p.G > 1);
         unsigned* c = counter_ptr(p, jb.rank, slot);
         if (atomicAdd(c, my_tiles) + my_tiles == unsigned(p.n_tiles)) {
             *c = 0u;
-            fence_sys();
-            st_release_sys(complete_ptr(p, jb.rank, slot), jb.version);
+            fence_sc(p.G > 1);
+            st_release_sc(p.G > 1, complete_ptr(p, jb.rank, slot), jb.version);
         }
     }
 }
