@@ -291,6 +291,13 @@ class DeviceContext:
             a.update_rule = _lib.WG_UPDATE_MOMENTUM if j.momentum else _lib.WG_UPDATE_SGD
             a.eta, a.beta = float(j.eta), float(j.beta)
             a.W, a.m, a.g, a.fresh, a.acc_out = _ptr(j.W), _ptr(j.m), _ptr(j.g), _ptr(j.fresh), _ptr(j.acc_out)
+        self.launch_array(arr, len(jobs), forced, stream)
+        if keep:  # realigned copies must outlive the asynchronous launch
+            torch.cuda.current_stream(self.torch_device).synchronize() if stream is None else stream.synchronize()
+
+    def launch_array(self, arr, n_jobs: int, forced: Optional[dict[int, Sequence[int]]] = None, stream=None) -> None:
+        """`wg_launch` on a prepared `WgJob` array (the optimizer's fast path;
+        the caller has validated every vector it points to)."""
         fv = fs = None
         nf = 0
         if forced:
@@ -303,12 +310,10 @@ class DeviceContext:
                     raise InvalidParamsError("forced stamp rows need P entries")
                 flat.extend(int(x) for x in st)
             fs = (ctypes.c_int64 * len(flat))(*flat)
-        rc = self.lib.wg_launch(self._h, arr, len(jobs), fv, fs, nf, self.stream_handle(stream))
+        rc = self.lib.wg_launch(self._h, arr, n_jobs, fv, fs, nf, self.stream_handle(stream))
         self._raise(rc, "wg_launch")
-        if keep:  # realigned copies must outlive the asynchronous launch
-            torch.cuda.current_stream(self.torch_device).synchronize() if stream is None else stream.synchronize()
         self.launches += 1
-        self._n_last = len(jobs)
+        self._n_last = n_jobs
 
     def statuses(self) -> list[JobStatus]:
         """Per-job status of the last launch (synchronise its stream first)."""

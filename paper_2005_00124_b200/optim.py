@@ -145,6 +145,11 @@ class GroupAveragingOptimizer:
             self.W[r] = w0.clone()
             self.m[r] = torch.zeros_like(w0) if self.momentum else None
             ctx.set_initial_model(r, w0)
+        # host fast path (step): the replicas are owned here, their pointers fixed
+        self._arr = None
+        self._slot: list = []
+        self._wptr = {r: w.data_ptr() for r, w in self.W.items()}
+        self._mptr = {r: (mm.data_ptr() if mm is not None else None) for r, mm in self.m.items()}
 
     def kind(self, t: int) -> int:
         if is_sync_iteration(t, self.cfg.tau):
@@ -170,11 +175,54 @@ class GroupAveragingOptimizer:
         flight (``ctx.check()`` after a synchronise is exact).
         """
         self.ctx.check_async()
-        versions = {r: t for r in grads}
         forced = {t: forced_stamps} if forced_stamps is not None else None
         if forced:
             self.forced_log.update(forced)
-        self.ctx.launch(self.jobs(versions, grads), forced=forced, stream=stream)
+        if not self._fast_step(t, grads, forced, stream):
+            self.ctx.launch(self.jobs({r: t for r in grads}, grads), forced=forced, stream=stream)
+
+    def _fast_step(self, t: int, grads: Mapping[int, torch.Tensor], forced, stream) -> bool:
+        """Host fast path of step(): a persistent job array (the optimizer's own
+        W / m, validated once) in which only the gradient pointer, version,
+        kind and step size change; each gradient is still checked (device,
+        dtype, size, contiguity, 16-byte alignment). Returns False (general
+        path) for a gradient that needs realigning."""
+        ctx = self.ctx
+        arr = self._arr
+        if arr is None or len(grads) > len(arr):
+            arr = self._arr = (_lib.WgJob * max(len(ctx.local_ranks), len(grads)))()
+            self._slot = [None] * len(arr)  # (rank, W ptr, m ptr) whose fixed fields a slot holds
+        kind = self.kind(t)
+        eta = float(self.cfg.eta.rate(t, ctx.P, self.T))
+        rule = _lib.WG_UPDATE_MOMENTUM if self.momentum else _lib.WG_UPDATE_SGD
+        dev, dt, n = ctx.torch_device, ctx.dtype, ctx.n
+        i = 0
+        for r, g in grads.items():
+            gp = g.data_ptr()
+            if gp % 16:
+                return False
+            if g.device != dev or g.dtype != dt or g.numel() != n or not g.is_contiguous():
+                ctx._check_vec(g, "g")  # raises with the message
+            wp = self.W[r].data_ptr()
+            if wp != self._wptr.get(r):  # a replica replaced by the caller: validate it once
+                ctx._check_vec(self.W[r], "W")
+                self._wptr[r] = wp
+            mm = self.m[r]
+            mp = mm.data_ptr() if mm is not None else None
+            if mp != self._mptr.get(r):
+                ctx._check_vec(mm, "m")
+                self._mptr[r] = mp
+            a = arr[i]
+            key = (r, wp, mp)
+            if self._slot[i] != key:
+                a.rank, a.update_rule, a.beta = r, rule, float(self.cfg.momentum)
+                a.W, a.m = wp, mp
+                a.fresh = a.acc_out = None
+                self._slot[i] = key
+            a.kind, a.version, a.eta, a.g = kind, t, eta, gp
+            i += 1
+        ctx.launch_array(arr, i, forced, stream)
+        return True
 
     def step_mixed(self, versions: Mapping[int, int], grads: Mapping[int, torch.Tensor],
                    forced: Optional[dict[int, list[int]]] = None, stream=None) -> None:
