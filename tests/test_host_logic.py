@@ -143,3 +143,62 @@ def test_fixed_victims_policy():
     assert pol.extra_delay_ms == 5.0
     with pytest.raises(ValueError):
         FixedVictims(4, 1.0).victims(0, 4)
+
+
+def test_optimizer_fast_step_job_array():
+    """GroupAveragingOptimizer.step's host fast path (no GPU: a stand-in context
+    records the wg_job array): per-step fields follow t (kind: sync every tau,
+    version, step size), fixed fields are rewritten when a replica is replaced,
+    gradients are validated, misaligned gradients fall back to the general path."""
+    import types
+
+    import torch
+
+    from paper_2005_00124_b200 import _lib
+    from paper_2005_00124_b200.optim import EtaSchedule, GroupAveragingOptimizer, OptimizerConfig
+    from paper_2005_00124_b200.topology import InvalidParamsError
+
+    n = 64
+    launched = []
+
+    class Ctx:
+        P, S, n, dtype = 4, 2, 64, torch.float32
+        torch_device = torch.device("cpu")
+        local_ranks = (0, 1)
+
+        def launch_array(self, arr, k, forced, stream):
+            launched.append([(arr[i].rank, arr[i].kind, arr[i].version, arr[i].eta, arr[i].W, arr[i].m, arr[i].g,
+                              arr[i].beta, arr[i].update_rule) for i in range(k)])
+
+        def _check_vec(self, t, name):
+            if t is not None and (t.dtype != self.dtype or t.numel() != self.n):
+                raise InvalidParamsError(name)
+
+    ctx = Ctx()
+    opt = object.__new__(GroupAveragingOptimizer)
+    opt.ctx, opt.cfg, opt.T = ctx, OptimizerConfig(T=10, S=2, tau=3, eta=EtaSchedule(value=0.25),
+                                                    update_rule="momentum", momentum=0.9), 10
+    opt.use_group, opt.momentum = True, True
+    opt.W = {r: torch.zeros(n) for r in ctx.local_ranks}
+    opt.m = {r: torch.zeros(n) for r in ctx.local_ranks}
+    opt._arr, opt._slot = None, []
+    opt._wptr = {r: w.data_ptr() for r, w in opt.W.items()}
+    opt._mptr = {r: w.data_ptr() for r, w in opt.m.items()}
+    g = {r: torch.ones(n) for r in ctx.local_ranks}
+    for t in range(3):
+        assert opt._fast_step(t, g, None, None)
+    kinds = [row[0][1] for row in launched]
+    assert kinds == [_lib.WG_JOB_STEP, _lib.WG_JOB_STEP, _lib.WG_JOB_SYNC_STEP]  # (t+1) % tau == 0
+    assert [row[0][2] for row in launched] == [0, 1, 2]
+    r0 = launched[-1][0]
+    assert r0[0] == 0 and r0[3] == 0.25 and r0[7] == 0.9 and r0[8] == _lib.WG_UPDATE_MOMENTUM
+    assert r0[4] == opt.W[0].data_ptr() and r0[5] == opt.m[0].data_ptr() and r0[6] == g[0].data_ptr()
+    # a replaced replica: its new pointer reaches the array
+    opt.W[1] = torch.full((n,), 2.0)
+    assert opt._fast_step(3, g, None, None)
+    assert launched[-1][1][4] == opt.W[1].data_ptr()
+    # a wrong-sized gradient is rejected; a misaligned one takes the general path
+    with pytest.raises(InvalidParamsError):
+        opt._fast_step(4, {0: torch.ones(n + 1)}, None, None)
+    misaligned = torch.ones(n + 1)[1:]
+    assert not opt._fast_step(4, {0: misaligned}, None, None)
