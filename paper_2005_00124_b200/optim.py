@@ -198,6 +198,8 @@ class GroupAveragingOptimizer:
         dev, dt, n = ctx.torch_device, ctx.dtype, ctx.n
         i = 0
         for r, g in grads.items():
+            if r not in self.W:
+                return False  # not a rank of this process: the general path reports it
             gp = g.data_ptr()
             if gp % 16:
                 return False
