@@ -20,7 +20,7 @@ import torch
 
 from . import _lib
 from .context import DeviceContext, DivergenceError, Job, JobStatus
-from .topology import GroupingParams
+from .topology import GroupingParams, InvalidParamsError
 
 __all__ = [
     "EtaSchedule",
@@ -199,7 +199,7 @@ class GroupAveragingOptimizer:
         i = 0
         for r, g in grads.items():
             if r not in self.W:
-                return False  # not a rank of this process: the general path reports it
+                raise InvalidParamsError(f"rank {r} is not hosted by this process")
             gp = g.data_ptr()
             if gp % 16:
                 return False

@@ -202,3 +202,5 @@ def test_optimizer_fast_step_job_array():
         opt._fast_step(4, {0: torch.ones(n + 1)}, None, None)
     misaligned = torch.ones(n + 1)[1:]
     assert not opt._fast_step(4, {0: misaligned}, None, None)
+    with pytest.raises(InvalidParamsError):  # not a rank of this process
+        opt._fast_step(4, {3: torch.ones(n)}, None, None)
