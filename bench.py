@@ -443,6 +443,11 @@ def run_ours(a):
     roof["t_star_frac"] = {"measured_peaks": max(t_hbm, t_nvl) / kern_s,
                            "nominal_900": max(t_hbm, nvl_b / (NVLINK_NOMINAL_GBS * 1e9)) / kern_s}
     roof["traffic"] = load_traffic(a, G)
+    roof["traffic_source"] = (
+        "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch)"
+        if roof["traffic"] is not None else
+        "none: ncu cannot wrap a multi-rank run and NVML NVLink/DRAM counters are not supported on this pool"
+        if G > 1 else "none: no committed ncu capture for this config")
     roof["algorithmic_bytes_per_launch"] = {"hbm": hbm_b, "nvlink_ingress": nvl_b}
     roof["kernel_ms"] = kern_avg_ms
     roof["roofline_ms"] = max(t_hbm, t_nvl) * 1e3
