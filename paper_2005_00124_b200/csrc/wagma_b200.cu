@@ -1210,9 +1210,12 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
 // ---------------------------------------------------------------------------
 // multi-GPU kernel: producer / puller / consumer warps
 //
-//  - 8 producer warps stream W, g, m through a per-thread cp.async ring, do the
-//    local step, install W' in the send ring and publish a per-warp flag per
-//    tile; they never wait on anything else, so they run ahead of the pulls.
+//  - 8 producer warps do the local step, install W' in the send ring and
+//    publish a per-warp flag per tile; their inputs W, g, m come from an
+//    issuer warp's TMA bulk copies into an mbarrier ring (>= 2 jobs per GPU,
+//    tma_produce) or from per-thread cp.async rings (one job per GPU,
+//    nvl_produce); they never wait on anything else, so they run ahead of the
+//    pulls.
 //  - 1 puller warp walks the same tiles: waits for every leaf's flag (peer
 //    GPUs over NVLink, and this GPU's own producers), then fetches each
 //    leaf-tile with one TMA bulk copy (cp.async.bulk global->shared; peer
@@ -1220,7 +1223,8 @@ __global__ void __launch_bounds__(kThreads, AHEAD ? WG_MINB_AHEAD : WG_MINB) wag
 //    are guarded by mbarriers (full: TMA bytes landed; empty: consumed).
 //  - 8 consumer warps sum the leaves of each plan from shared memory in the
 //    butterfly order and write W_{t+1}.
-// One 544-thread CTA per SM; stage count chosen from the shared-memory budget.
+// One 576-thread CTA per SM (+ the issuer warp); stage count chosen from the
+// shared-memory budget.
 // ---------------------------------------------------------------------------
 
 #ifndef WG_NVL_DEPTH
